@@ -1,0 +1,198 @@
+/*
+ * convlinear4bit.h -- the drop-in C-ABI of the B200-native ConvLinear4bit
+ * forward path (one shared library: paper_2512_03673_b200/libconvrot_b200.so).
+ *
+ * The reference (/root/reference/proj) is a C++20 library with no C or FFI
+ * surface; each entry point below replaces one reference function on the
+ * ConvLinear4bit hot path and keeps its argument meaning
+ * and error behaviour.  Reference paths are relative to /root/reference/proj.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Pointers documented "device" must be
+ *     CUDA device (or managed) memory; "host" pointers are CPU memory
+ *     (pinned memory makes the *_host entry points asynchronous-capable).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *     All device work is stream-ordered; no entry point synchronises unless
+ *     documented.
+ *   - Shape / order / divisibility / capacity errors are detected on the
+ *     host before any launch and returned synchronously.  Data-dependent
+ *     errors (non-finite input, reference: compute_scales throws
+ *     InvalidValueError, quant.cpp:16-18) set a device error word that
+ *     crt_device_status() reports.
+ *   - crt_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef CRT_CONVLINEAR4BIT_H_
+#define CRT_CONVLINEAR4BIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CRT_ABI_VERSION 1
+
+/* Status codes, 1:1 with the reference exception taxonomy (errors.hpp:9-67). */
+typedef enum crt_status {
+  CRT_OK = 0,
+  CRT_ERR_INVALID_ORDER = 1, /* InvalidOrderError (errors.hpp:18-22) */
+  CRT_ERR_INVALID_VALUE = 2, /* InvalidValueError (errors.hpp:24-29) */
+  CRT_ERR_SHAPE = 3,         /* ShapeError        (errors.hpp:31-35) */
+  CRT_ERR_CAPACITY = 4,      /* CapacityError     (errors.hpp:37-41) */
+  CRT_ERR_FORMAT = 5,        /* FormatError       (errors.hpp:43-54) */
+  CRT_ERR_CUDA = 6,          /* CUDA runtime/driver failure */
+  CRT_ERR_UNSUPPORTED = 7    /* valid for the reference, not built here */
+} crt_status;
+
+/* RotationKind (pipeline.hpp:14); random_orthogonal is out of scope. */
+typedef enum crt_rotation_kind {
+  CRT_ROT_NONE = 0,
+  CRT_ROT_SYLVESTER = 1,
+  CRT_ROT_REGULAR = 2
+} crt_rotation_kind;
+
+/* Element types of the activations / weights handed to the library. */
+typedef enum crt_dtype {
+  CRT_DTYPE_BF16 = 0,
+  CRT_DTYPE_F32 = 1
+} crt_dtype;
+
+/* Output flavours of the GEMM epilogue. */
+typedef enum crt_out_kind {
+  CRT_OUT_BF16 = 0,    /* y = acc*s_a*s_w + b, rounded to bf16 (production) */
+  CRT_OUT_F32 = 1,     /* same in fp32 (dequant parity, pipeline.cpp:224-230) */
+  CRT_OUT_I32_ACC = 2  /* raw int32 accumulators (int_gemm parity, :178-204) */
+} crt_out_kind;
+
+/* RotationSpec (pipeline.hpp:23-30).  group_size 0 = global (one block
+ * spanning K, pipeline.cpp:120-122).  seed is accepted for layout parity
+ * (random_orthogonal only in the reference) and ignored. */
+typedef struct crt_rotation_spec {
+  int32_t kind;
+  int32_t group_size;
+  uint64_t seed;
+  int32_t identity_tail;
+} crt_rotation_spec;
+
+/* -------------------------------------------------------------------------
+ * a1: regular(n) -- replaces convrot::regular (hadamard.cpp:91-106) and the
+ * Kronecker rule of convrot::kronecker (hadamard.cpp:108-126).  Writes the
+ * n x n sign matrix (+1/-1, row-major) to HOST memory.  INVALID_ORDER unless
+ * n is a power of four in [4, 4096] (hadamard.cpp:92-96). */
+crt_status crt_regular_hadamard(int32_t n, int8_t* signs_host);
+
+/* Sylvester sign matrix (hadamard.cpp:70-89), power of two <= 4096. */
+crt_status crt_sylvester_hadamard(int32_t n, int8_t* signs_host);
+
+/* -------------------------------------------------------------------------
+ * K1: group_rotate + compute_scales + quantize + pack_int4 --
+ * replaces pipeline.cpp:111-151 (group_rotate), quant.cpp:10-24
+ * (compute_scales), quant.cpp:26-52 (quantize) and quant.cpp:64-81
+ * (pack_int4), i.e. the activation half of forward (pipeline.cpp:216-218).
+ *
+ *   x        device, M rows x K, row stride ldx ELEMENTS, dtype x_dtype
+ *   rot      rotation spec (kind none/regular; sylvester accepted)
+ *   bits     4 (codes nibble-packed exactly as pack_int4: element 2t in the
+ *            low nibble of byte t, rows padded to a whole byte) or 8 (int8)
+ *   codes    device, M rows x ld_codes BYTES (>= ceil(K/2) for bits 4,
+ *            >= K for bits 8)
+ *   scales_f32 device, M floats, (float)s           (nullable)
+ *   scales_f64 device, M doubles, s exactly as compute_scales (nullable)
+ *
+ * Codes and the f64 scales are bit-identical to the reference's
+ * quantize(group_rotate(x)) / compute_scales on the same inputs widened to
+ * double. */
+crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K,
+                            int64_t ldx, const crt_rotation_spec* rot, int32_t bits,
+                            uint8_t* codes, int64_t ld_codes, float* scales_f32,
+                            double* scales_f64, void* stream);
+
+/* -------------------------------------------------------------------------
+ * K2: prepare_layer -- replaces pipeline.cpp:158-176.  Rotates W (N x K,
+ * device, row stride ldw elements) along K, quantizes per output channel and
+ * stores the codes in the K3 tile layout inside an opaque, immutable layer
+ * handle that owns all its device memory.  bias is device fp32 (N) or NULL.
+ * The reference's bias-length check (pipeline.cpp:162-164) is implicit: the
+ * bias is read as N values. */
+typedef struct crt_layer crt_layer;
+
+typedef struct crt_layer_desc {
+  int64_t out_features; /* N */
+  int64_t in_features;  /* K */
+  crt_rotation_spec rotation;
+  int32_t bits_w;       /* 4 or 8 (QuantSpec, quant.hpp:15-20) */
+  int32_t w_dtype;      /* crt_dtype of W */
+} crt_layer_desc;
+
+crt_status crt_layer_prepare(const crt_layer_desc* desc, const void* w, int64_t ldw,
+                             const float* bias, void* stream, crt_layer** out);
+
+/* Column-parallel shard of a layer: output channels
+ * [rank*N/nranks, (rank+1)*N/nranks) of the full W.
+ * Codes and scales equal the corresponding rows of the full layer. */
+crt_status crt_layer_prepare_shard(const crt_layer_desc* desc, const void* w,
+                                   int64_t ldw, const float* bias, int32_t rank,
+                                   int32_t nranks, void* stream, crt_layer** out);
+
+crt_status crt_layer_destroy(crt_layer* layer);
+
+/* Geometry of a prepared layer (host query). */
+crt_status crt_layer_info(const crt_layer* layer, crt_layer_desc* desc_out);
+
+/* Export the prepared weights in the reference layout for parity checks:
+ * codes row-major packed like pack_int4 (bits 4) or int8 (bits 8), ld_codes
+ * bytes per row; per-channel scales as f32 and/or f64 (nullable). Device. */
+crt_status crt_layer_export(const crt_layer* layer, uint8_t* codes, int64_t ld_codes,
+                            float* scales_f32, double* scales_f64, void* stream);
+
+/* -------------------------------------------------------------------------
+ * K3: int_gemm + dequant -- replaces pipeline.cpp:178-204 (int_gemm, with
+ * its CapacityError precheck :184-192) and the dequant loop of forward
+ * (pipeline.cpp:224-230).
+ *
+ *   a_codes   device, K1 output (M rows, lda BYTES per row, bits_a layout)
+ *   a_scales  device, M fp32 activation scales
+ *   y         device, M x N (ldy ELEMENTS) of bf16 / f32 / int32 per out_kind
+ */
+crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                          int32_t bits_a, const crt_layer* layer, int64_t M,
+                          int32_t out_kind, void* y, int64_t ldy, void* stream);
+
+/* -------------------------------------------------------------------------
+ * a9: forward -- replaces pipeline.cpp:206-233: K1 on x, then K3 against the
+ * layer.  bits_a in {4, 8} else INVALID_VALUE (:213-215); x must have
+ * in_features columns else SHAPE (:208-212).  The workspace holds the
+ * activation codes/scales (no hidden allocation on the forward path). */
+typedef struct crt_workspace crt_workspace;
+
+crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** out);
+crt_status crt_workspace_destroy(crt_workspace* ws);
+
+crt_status crt_forward(const crt_layer* layer, const void* x, int32_t x_dtype,
+                       int64_t M, int64_t ldx, int32_t bits_a, int32_t out_kind,
+                       void* y, int64_t ldy, crt_workspace* ws, void* stream);
+
+/* forward with HOST buffers: copies x host->device, runs crt_forward and
+ * copies y device->host, all on `stream`; synchronises the stream before
+ * returning.  x_dev/y_dev are caller-owned device staging buffers. */
+crt_status crt_forward_host(const crt_layer* layer, const void* x_host, int32_t x_dtype,
+                            int64_t M, int32_t bits_a, int32_t out_kind, void* y_host,
+                            void* x_dev, void* y_dev, crt_workspace* ws, void* stream);
+
+/* -------------------------------------------------------------------------
+ * Diagnostics. */
+const char* crt_last_error(void);
+/* Synchronises `stream`, returns CRT_ERR_INVALID_VALUE if a kernel saw a
+ * non-finite input since the last reset (reference: compute_scales throws
+ * InvalidValueError, quant.cpp:16-18), then clears the word if reset != 0. */
+crt_status crt_device_status(void* stream, int32_t reset);
+/* Number of CUDA kernels this library has launched (process lifetime). */
+int64_t crt_launch_count(void);
+int32_t crt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRT_CONVLINEAR4BIT_H_ */

@@ -1,0 +1,308 @@
+"""Torch-level mirror of the reference operator surface for the
+ConvLinear4bit path (reference: /root/reference/proj/core/include/convrot/
+{hadamard,quant,pipeline}.hpp).  Names, argument meaning and error classes
+follow the reference; tensors are CUDA tensors and every call goes through
+the C-ABI (``_abi.py`` -> libconvrot_b200.so).  PyTorch only supplies device
+memory and the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import (CapacityError, CudaError, Error, FormatError, InvalidOrderError,  # noqa: F401
+                   InvalidValueError, ShapeError, UnsupportedError, check)
+
+
+class RotationKind(enum.IntEnum):
+    """pipeline.hpp:14 (random_orthogonal is out of scope here)."""
+    none = 0
+    sylvester = 1
+    regular = 2
+
+
+@dataclass(frozen=True)
+class RotationSpec:
+    """pipeline.hpp:23-30.  group_size 0 = global (one block over K)."""
+    kind: RotationKind = RotationKind.none
+    group_size: int = 0
+    seed: int = 0
+    identity_tail: bool = False
+
+    def c(self) -> _abi.RotationSpecC:
+        return _abi.RotationSpecC(int(self.kind), int(self.group_size), int(self.seed),
+                                  int(self.identity_tail))
+
+
+@dataclass(frozen=True)
+class QuantSpec:
+    """quant.hpp:15-20: symmetric per-row quantizer, codes in [-qmax, qmax]."""
+    bits: int = 4
+
+    def qmax(self) -> int:
+        return (1 << (self.bits - 1)) - 1
+
+
+_OUT = {"bf16": _abi.CRT_OUT_BF16, "f32": _abi.CRT_OUT_F32, "i32": _abi.CRT_OUT_I32_ACC}
+_OUT_DTYPE = {"bf16": torch.bfloat16, "f32": torch.float32, "i32": torch.int32}
+
+
+def _lib():
+    return _abi.load()
+
+
+def _stream(t: Optional[torch.Tensor] = None) -> ctypes.c_void_p:
+    dev = t.device if t is not None else torch.device("cuda")
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _abi.CRT_DTYPE_BF16
+    if t.dtype == torch.float32:
+        return _abi.CRT_DTYPE_F32
+    raise InvalidValueError(f"unsupported input dtype {t.dtype} (bf16 or f32)")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check_2d_cuda(x: torch.Tensor, what: str) -> None:
+    if not x.is_cuda:
+        raise InvalidValueError(f"{what} must be a CUDA tensor")
+    if x.dim() != 2:
+        raise ShapeError(f"{what} must be 2-D")
+    if x.stride(1) != 1:
+        raise ShapeError(f"{what} must be row-major with unit column stride")
+
+
+# ---------------------------------------------------------------------------
+# a1: Hadamard construction (hadamard.cpp:70-126)
+# ---------------------------------------------------------------------------
+def regular(n: int) -> np.ndarray:
+    """Regular Hadamard sign matrix H_n = H4^{(x)log4 n} (hadamard.cpp:91-106)."""
+    out = np.empty((n, n) if 0 < n <= 4096 else (1,), np.int8)
+    check(_lib().crt_regular_hadamard(n, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def sylvester(n: int) -> np.ndarray:
+    out = np.empty((n, n) if 0 < n <= 4096 else (1,), np.int8)
+    check(_lib().crt_sylvester_hadamard(n, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# K1: group_rotate -> compute_scales -> quantize -> pack_int4
+# ---------------------------------------------------------------------------
+def packed_row_bytes(k: int, bits: int) -> int:
+    return (k + 1) // 2 if bits == 4 else k
+
+
+def rotate_quantize(x: torch.Tensor, rotation: RotationSpec, aq: QuantSpec = QuantSpec(4),
+                    *, scales64: bool = False, check_finite: bool = True):
+    """Fused group_rotate + compute_scales + quantize + pack_int4 on the GPU.
+
+    Returns ``(codes, scales_f32[, scales_f64])``: codes is uint8
+    [M, ld] with the reference nibble layout in the first ceil(K/2) bytes of
+    each row (bits 4) or int8 codes (bits 8).  Bit-identical to the
+    reference's quantize(group_rotate(x)) codes and compute_scales."""
+    _check_2d_cuda(x, "x")
+    M, K = x.shape
+    row = packed_row_bytes(K, aq.bits)
+    ld = max(16, (row + 15) // 16 * 16)
+    codes = torch.empty((M, ld), dtype=torch.uint8, device=x.device)
+    s32 = torch.empty(M, dtype=torch.float32, device=x.device)
+    s64 = torch.empty(M, dtype=torch.float64, device=x.device) if scales64 else None
+    rc = rotation.c()
+    st = _stream(x)
+    check(_lib().crt_rotate_quant(_ptr(x), _dtype_code(x), M, K, x.stride(0), ctypes.byref(rc),
+                                  aq.bits, _ptr(codes), ld, _ptr(s32), _ptr(s64), st))
+    if check_finite:
+        check(_lib().crt_device_status(st, 1))
+    return (codes, s32, s64) if scales64 else (codes, s32)
+
+
+# ---------------------------------------------------------------------------
+# K2: prepare_layer (pipeline.cpp:158-176)
+# ---------------------------------------------------------------------------
+class PreparedLayer:
+    """Offline-rotated, offline-quantized weights (pipeline.hpp:55-65), owned
+    on the device by an immutable C-ABI handle."""
+
+    def __init__(self, handle: int, out_features: int, in_features: int, rotation: RotationSpec,
+                 weight_quant: QuantSpec, has_bias: bool, name: str, device: torch.device,
+                 shard: Tuple[int, int] = (0, 1)):
+        self._h = ctypes.c_void_p(handle)
+        self.out_features = out_features
+        self.in_features = in_features
+        self.rotation = rotation
+        self.weight_quant = weight_quant
+        self.has_bias = has_bias
+        self.name = name
+        self.device = device
+        self.shard = shard
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._h is None or not self._h.value:
+            raise Error("layer destroyed")
+        return self._h
+
+    def export(self, scales64: bool = True):
+        """(codes [N, ceil(K/2)] uint8 packed like pack_int4 (or int8 rows for
+        8-bit), scales f32, scales f64) -- the reference layout."""
+        N, K = self.out_features, self.in_features
+        row = packed_row_bytes(K, self.weight_quant.bits)
+        codes = torch.empty((N, max(row, 1)), dtype=torch.uint8, device=self.device)
+        s32 = torch.empty(N, dtype=torch.float32, device=self.device)
+        s64 = torch.empty(N, dtype=torch.float64, device=self.device) if scales64 else None
+        with torch.cuda.device(self.device):
+            check(_lib().crt_layer_export(self.handle, _ptr(codes), max(row, 1), _ptr(s32),
+                                          _ptr(s64), _stream()))
+        return (codes[:, :row], s32, s64) if scales64 else (codes[:, :row], s32)
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            _lib().crt_layer_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _prepare(w, bias, rotation, wq, name, rank, nranks):
+    _check_2d_cuda(w, "w")
+    if not w.is_contiguous() and w.stride(1) != 1:
+        raise ShapeError("w must be row-major")
+    N, K = w.shape
+    if bias is not None:
+        if bias.numel() != N:  # pipeline.cpp:162-164
+            raise ShapeError("prepare_layer: bias length must equal out_features")
+        bias = bias.to(device=w.device, dtype=torch.float32).contiguous()
+    desc = _abi.LayerDescC(N, K, rotation.c(), wq.bits, _dtype_code(w))
+    h = ctypes.c_void_p()
+    with torch.cuda.device(w.device):
+        st = _stream(w)
+        if nranks == 1:
+            check(_lib().crt_layer_prepare(ctypes.byref(desc), _ptr(w), w.stride(0), _ptr(bias),
+                                           st, ctypes.byref(h)))
+        else:
+            check(_lib().crt_layer_prepare_shard(ctypes.byref(desc), _ptr(w), w.stride(0),
+                                                 _ptr(bias), rank, nranks, st, ctypes.byref(h)))
+        check(_lib().crt_device_status(st, 1))
+    return PreparedLayer(h.value, N // nranks, K, rotation, wq, bias is not None, name, w.device,
+                         (rank, nranks))
+
+
+def prepare_layer(w: torch.Tensor, bias: Optional[torch.Tensor], rotation: RotationSpec,
+                  wq: QuantSpec = QuantSpec(4), name: str = "") -> PreparedLayer:
+    return _prepare(w, bias, rotation, wq, name, 0, 1)
+
+
+def prepare_layer_shard(w: torch.Tensor, bias: Optional[torch.Tensor], rotation: RotationSpec,
+                        wq: QuantSpec, rank: int, nranks: int, name: str = "") -> PreparedLayer:
+    """Column-parallel shard: output channels [rank*N/P, (rank+1)*N/P)."""
+    return _prepare(w, bias, rotation, wq, name, rank, nranks)
+
+
+# ---------------------------------------------------------------------------
+# K3 + forward (pipeline.cpp:178-233)
+# ---------------------------------------------------------------------------
+class Workspace:
+    """Activation codes/scales scratch for forward (no hidden allocations)."""
+
+    def __init__(self, max_m: int, max_k: int, device=None):
+        self.max_m, self.max_k = max_m, max_k
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(_lib().crt_workspace_create(max_m, max_k, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _lib().crt_workspace_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ws_cache = {}
+
+
+def _workspace_for(M: int, K: int, device) -> Workspace:
+    key = (str(device),)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.max_m < M or ws.max_k < K:
+        ws = Workspace(max(M, ws.max_m if ws else 0), max(K, ws.max_k if ws else 0), device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def forward(x: torch.Tensor, layer: PreparedLayer, aq: QuantSpec = QuantSpec(4), *,
+            out: str = "bf16", y: Optional[torch.Tensor] = None,
+            workspace: Optional[Workspace] = None, check_finite: bool = False) -> torch.Tensor:
+    """Online half of ConvLinear4bit (pipeline.cpp:206-233): rotate x,
+    per-token quantize, integer GEMM against the prepared weights, dequantize
+    by s_a[m]*s_w[n], add bias.  ``out``: "bf16" (production), "f32"
+    (dequant parity) or "i32" (raw int_gemm accumulators)."""
+    _check_2d_cuda(x, "x")
+    M, K = x.shape
+    if K != layer.in_features:  # pipeline.cpp:208-212
+        raise ShapeError(f"forward: input has {K} columns, layer expects {layer.in_features}")
+    if aq.bits not in (4, 8):  # :213-215
+        raise InvalidValueError("forward: activation bits must be 4 or 8")
+    N = layer.out_features
+    if y is None:
+        y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=x.device)
+    ws = workspace or _workspace_for(M, K, x.device)
+    st = _stream(x)
+    check(_lib().crt_forward(layer.handle, _ptr(x), _dtype_code(x), M, x.stride(0), aq.bits,
+                             _OUT[out], _ptr(y), y.stride(0), ws.handle, st))
+    if check_finite:
+        check(_lib().crt_device_status(st, 1))
+    return y
+
+
+def quant_gemm(codes: torch.Tensor, scales: torch.Tensor, layer: PreparedLayer,
+               aq: QuantSpec = QuantSpec(4), *, out: str = "bf16",
+               y: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """int_gemm + dequant on pre-quantized activations (K1 output)."""
+    M = codes.shape[0]
+    N = layer.out_features
+    if y is None:
+        y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=codes.device)
+    check(_lib().crt_quant_gemm(_ptr(codes), codes.stride(0), _ptr(scales), aq.bits, layer.handle,
+                                M, _OUT[out], _ptr(y), y.stride(0), _stream(codes)))
+    return y
+
+
+def int_gemm(codes: torch.Tensor, layer: PreparedLayer, aq: QuantSpec = QuantSpec(4)):
+    """Raw int32 accumulators (int_gemm, pipeline.cpp:178-204) of packed
+    activation codes against the prepared weights."""
+    ones = torch.ones(codes.shape[0], dtype=torch.float32, device=codes.device)
+    return quant_gemm(codes, ones, layer, aq, out="i32")
+
+
+def launch_count() -> int:
+    """Kernels this library has launched so far (process lifetime)."""
+    return int(_lib().crt_launch_count())

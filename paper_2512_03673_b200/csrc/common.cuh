@@ -1,0 +1,77 @@
+// common.cuh -- shared device helpers for the sm_100a ConvLinear4bit kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace crt {
+
+enum : int { kRotNone = 0, kRotSylvester = 1, kRotRegular = 2 };
+
+// Device error word (passed by pointer): set by a kernel that sees a
+// non-finite input -- the reference throws InvalidValueError from
+// compute_scales (quant.cpp:16-18).
+__device__ __forceinline__ void flag_invalid_value(int* err) { atomicOr(err, 1); }
+
+// ---- packed fp32x2 arithmetic (FADD2 / FFMA2 on sm_100) -------------------
+__device__ __forceinline__ uint64_t f2_bits(float2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_from(uint64_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+// a * b + c, one rounding per lane
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(r);
+}
+
+// NaN-propagating max of |a|, |b| and c (FMNMX3.NAN with abs modifiers).
+__device__ __forceinline__ float max3_abs(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(fabsf(a)), "f"(fabsf(b)), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// 256-bit streaming load (LDG.E.NA.ENL2.256): 8 words, no L1 allocation.
+__device__ __forceinline__ void ld_nc_v8(const void* p, uint32_t (&v)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+        "=r"(v[6]), "=r"(v[7])
+      : "l"(p));
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Sign of entry (k, j) of the order-4^L regular Hadamard matrix:
+// H = H4^{(x)L} with H4[a][b] = -1 iff a + b == 3 (hadamard.cpp:97-102,119);
+// per base-4 digit, a + b == 3  <=>  (a ^ b) == 3.
+__device__ __forceinline__ bool regular_negative(uint32_t k, uint32_t j) {
+  uint32_t d = k ^ j;
+  return (__popc(d & (d >> 1) & 0x55555555u) & 1u) != 0;
+}
+// Sylvester (hadamard.cpp:70-89): H[k][j] = (-1)^popcount(k & j).
+__device__ __forceinline__ bool sylvester_negative(uint32_t k, uint32_t j) {
+  return (__popc(k & j) & 1u) != 0;
+}
+
+}  // namespace crt

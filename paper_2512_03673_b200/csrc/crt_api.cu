@@ -1,0 +1,417 @@
+// crt_api.cu -- the C-ABI (include/crt/convlinear4bit.h): host-side
+// validation with the reference's error behaviour, resource ownership, and
+// the launches of K1 (rotate+quant), K2 (weight prep) and K3 (GEMM).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/crt/convlinear4bit.h"
+#include "common.cuh"
+#include "k1_rotate_quant.h"
+#include "k3_gemm.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+// One device error word per device (lazily allocated, never freed).
+int* device_error_word() {
+  static int* words[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!words[dev]) {
+    int* p = nullptr;
+    if (cudaMalloc(&p, sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, sizeof(int));
+    cudaDeviceSynchronize();
+    words[dev] = p;
+  }
+  return words[dev];
+}
+
+crt_status fail(crt_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+crt_status cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return CRT_ERR_CUDA;
+}
+
+bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+bool is_pow4(int64_t n) { return is_pow2(n) && (n & 0x5555555555555555LL) != 0; }
+
+// Resolve and validate a rotation spec against a width the way group_rotate
+// does (pipeline.cpp:111-130, check_group_order :27-50).  On success
+// *group is the block width (1 for kind none) and *rot_cols the columns
+// covered by whole blocks.
+crt_status resolve_rotation(const crt_rotation_spec* rot, int64_t cols, int64_t* group,
+                            int64_t* rot_cols) {
+  crt_rotation_spec none{CRT_ROT_NONE, 0, 0, 0};
+  if (rot == nullptr) rot = &none;
+  if (rot->kind == CRT_ROT_NONE) {  // :114 returns x unchanged, no checks
+    *group = 1;
+    *rot_cols = cols;
+    return CRT_OK;
+  }
+  if (rot->kind != CRT_ROT_REGULAR && rot->kind != CRT_ROT_SYLVESTER)
+    return fail(CRT_ERR_UNSUPPORTED, "rotation kind not supported (random_orthogonal is out of scope)");
+  if (cols == 0) return fail(CRT_ERR_SHAPE, "group_rotate: empty input");
+  if (rot->group_size < 0) return fail(CRT_ERR_INVALID_VALUE, "group_rotate: negative group size");
+  int64_t g = rot->group_size == 0 ? cols : rot->group_size;
+  if (rot->kind == CRT_ROT_SYLVESTER && !is_pow2(g))
+    return fail(CRT_ERR_INVALID_ORDER,
+                "sylvester rotation needs a power-of-two group size, got " + std::to_string(g));
+  if (rot->kind == CRT_ROT_REGULAR && (!is_pow4(g) || g < 4))
+    return fail(CRT_ERR_INVALID_ORDER,
+                "regular rotation needs a power-of-four group size, got " + std::to_string(g));
+  if (g > 4096)  // hadamard.hpp:12 kMaxHadamardOrder
+    return fail(CRT_ERR_INVALID_ORDER, "order " + std::to_string(g) + " exceeds maximum 4096");
+  int64_t blocks = cols / g;
+  if (blocks * g != cols && !rot->identity_tail)
+    return fail(CRT_ERR_SHAPE, "group_rotate: " + std::to_string(cols) +
+                                   " columns not divisible by group size " + std::to_string(g));
+  *group = g;
+  *rot_cols = blocks * g;
+  return CRT_OK;
+}
+
+crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
+                  const crt_rotation_spec* rot, int32_t bits, uint8_t* codes, int64_t ldc,
+                  float* s32, double* s64, cudaStream_t st) {
+  if (x_dtype != CRT_DTYPE_BF16 && x_dtype != CRT_DTYPE_F32)
+    return fail(CRT_ERR_INVALID_VALUE, "unsupported input dtype");
+  if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
+  if (M < 0 || K < 0) return fail(CRT_ERR_SHAPE, "negative shape");
+  int64_t group = 1, rot_cols = K;
+  crt_status rs = resolve_rotation(rot, K, &group, &rot_cols);
+  if (rs != CRT_OK) return rs;
+  if (M == 0) return CRT_OK;
+  if (K == 0) {  // reference: zero-width rows -> scale 1.0, no codes
+    std::vector<float> ones32(M, 1.f);
+    std::vector<double> ones64(M, 1.0);
+    if (s32) cudaMemcpyAsync(s32, ones32.data(), M * 4, cudaMemcpyHostToDevice, st);
+    if (s64) cudaMemcpyAsync(s64, ones64.data(), M * 8, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+    return CRT_OK;
+  }
+  if (ldx < K) return fail(CRT_ERR_SHAPE, "ldx < K");
+  const int64_t row_bytes = bits == 4 ? (K + 1) / 2 : K;
+  if (ldc < row_bytes) return fail(CRT_ERR_SHAPE, "ld_codes too small for one packed row");
+  if (x == nullptr || codes == nullptr) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
+  const bool f32 = x_dtype == CRT_DTYPE_F32;
+  const int kind = rot ? rot->kind : CRT_ROT_NONE;
+  crt::K1Args a{};
+  a.x = x;
+  a.ldx = ldx;
+  a.M = M;
+  a.K = K;
+  a.group = group;
+  a.rot_cols = rot_cols;
+  a.kind = kind;
+  a.codes = codes;
+  a.ldc = ldc;
+  a.s32 = s32;
+  a.s64 = s64;
+  a.err = device_error_word();
+  if (!a.err) return fail(CRT_ERR_CUDA, "device error word allocation failed");
+  crt::K1Plan plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx,
+                                  codes, ldc);
+  int64_t launches = 0;
+  cudaError_t e = crt::launch_k1(a, plan, f32, bits, st, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess) return cuda_fail(e, "rotate_quant launch");
+  return CRT_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct crt_layer {
+  crt_layer_desc desc;
+  int64_t n_total;      // N of the full layer (== desc.out_features unless sharded)
+  int64_t row_offset;   // first output channel of this shard
+  uint8_t* codes;       // N x ldc, reference row layout (packed int4 / int8)
+  int64_t ldc;
+  float* s32;           // N
+  double* s64;          // N
+  float* bias;          // N or null
+  crt::K3Weights tiles; // K3 operand layout
+};
+
+struct crt_workspace {
+  int64_t max_m, max_k;
+  uint8_t* codes;
+  float* s32;
+};
+
+extern "C" {
+
+int32_t crt_abi_version(void) { return CRT_ABI_VERSION; }
+const char* crt_last_error(void) { return g_err.c_str(); }
+int64_t crt_launch_count(void) { return g_launches.load(); }
+
+// hadamard.cpp:91-106 / :108-126.  H_{4^L}[r][c] = prod_s H4[r_s][c_s]; the
+// Kronecker rule puts the right factor on the least significant base-4
+// digit, and H4[a][b] = -1 iff a + b == 3.
+crt_status crt_regular_hadamard(int32_t n, int8_t* signs) {
+  if (!is_pow4(n) || n < 4)
+    return fail(CRT_ERR_INVALID_ORDER,
+                "regular: order must be a power of four >= 4, got " + std::to_string(n));
+  if (n > 4096) return fail(CRT_ERR_INVALID_ORDER, "regular: order exceeds maximum 4096");
+  if (!signs) return fail(CRT_ERR_INVALID_VALUE, "null output");
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t c = 0; c < n; ++c) {
+      uint32_t d = (uint32_t)(r ^ c);
+      int neg = __builtin_popcount(d & (d >> 1) & 0x55555555u) & 1;
+      signs[(int64_t)r * n + c] = neg ? -1 : 1;
+    }
+  return CRT_OK;
+}
+
+// hadamard.cpp:70-89: H[r][c] = (-1)^popcount(r & c).
+crt_status crt_sylvester_hadamard(int32_t n, int8_t* signs) {
+  if (!is_pow2(n)) return fail(CRT_ERR_INVALID_ORDER, "sylvester: order must be a power of two");
+  if (n > 4096) return fail(CRT_ERR_INVALID_ORDER, "sylvester: order exceeds maximum 4096");
+  if (!signs) return fail(CRT_ERR_INVALID_VALUE, "null output");
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t c = 0; c < n; ++c)
+      signs[(int64_t)r * n + c] = (__builtin_popcount((uint32_t)(r & c)) & 1) ? -1 : 1;
+  return CRT_OK;
+}
+
+crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
+                            const crt_rotation_spec* rot, int32_t bits, uint8_t* codes,
+                            int64_t ld_codes, float* scales_f32, double* scales_f64,
+                            void* stream) {
+  return run_k1(x, x_dtype, M, K, ldx, rot, bits, codes, ld_codes, scales_f32, scales_f64,
+                (cudaStream_t)stream);
+}
+
+crt_status crt_device_status(void* stream, int32_t reset) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "device_status sync");
+  int v = 0;
+  int* word = device_error_word();
+  if (!word) return fail(CRT_ERR_CUDA, "device error word allocation failed");
+  e = cudaMemcpy(&v, word, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "device_status read");
+  if (reset && v) cudaMemset(word, 0, sizeof(int));
+  if (v) return fail(CRT_ERR_INVALID_VALUE, "compute_scales: non-finite input");
+  return CRT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2: prepare_layer (pipeline.cpp:158-176)
+// ---------------------------------------------------------------------------
+static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t ldw,
+                               const float* bias, int32_t rank, int32_t nranks,
+                               cudaStream_t st, crt_layer** out) {
+  if (!d || !out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
+  *out = nullptr;
+  if (d->bits_w != 4 && d->bits_w != 8) return fail(CRT_ERR_INVALID_VALUE, "bits_w must be 4 or 8");
+  if (d->out_features < 0 || d->in_features < 0) return fail(CRT_ERR_SHAPE, "negative shape");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(CRT_ERR_INVALID_VALUE, "bad rank / nranks");
+  const int64_t N = d->out_features, K = d->in_features;
+  if (N % nranks != 0) return fail(CRT_ERR_SHAPE, "out_features not divisible by nranks");
+  const int64_t Ns = N / nranks, off = (int64_t)rank * Ns;
+  int64_t group = 1, rot_cols = K;
+  crt_status rs = resolve_rotation(&d->rotation, K, &group, &rot_cols);
+  if (rs != CRT_OK) return rs;
+  const int esz = d->w_dtype == CRT_DTYPE_F32 ? 4 : 2;
+  crt_layer* L = new crt_layer();
+  L->desc = *d;
+  L->desc.out_features = Ns;
+  L->n_total = N;
+  L->row_offset = off;
+  L->ldc = d->bits_w == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
+  cudaError_t e = cudaSuccess;
+  size_t nalloc = (size_t)(Ns ? Ns : 1);
+  if (e == cudaSuccess) e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
+  if (e == cudaSuccess && bias) {
+    e = cudaMalloc(&L->bias, 4 * nalloc);
+    if (e == cudaSuccess && Ns)
+      e = cudaMemcpyAsync(L->bias, bias + off, 4 * Ns, cudaMemcpyDeviceToDevice, st);
+  }
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "layer alloc");
+  }
+  // K1 on the weight rows: rotation along K, per-output-channel scales.
+  const char* wbase = reinterpret_cast<const char*>(w) + off * ldw * esz;
+  crt_status s = run_k1(wbase, d->w_dtype, Ns, K, ldw, &d->rotation, d->bits_w, L->codes, L->ldc,
+                        L->s32, L->s64, st);
+  if (s != CRT_OK) {
+    crt_layer_destroy(L);
+    return s;
+  }
+  int64_t launches = 0;
+  e = crt::k3_prepare_weights(L->codes, L->ldc, Ns, K, d->bits_w, &L->tiles, st, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "weight tiling");
+  }
+  *out = L;
+  return CRT_OK;
+}
+
+crt_status crt_layer_prepare(const crt_layer_desc* desc, const void* w, int64_t ldw,
+                             const float* bias, void* stream, crt_layer** out) {
+  return prepare_impl(desc, w, ldw, bias, 0, 1, (cudaStream_t)stream, out);
+}
+
+crt_status crt_layer_prepare_shard(const crt_layer_desc* desc, const void* w, int64_t ldw,
+                                   const float* bias, int32_t rank, int32_t nranks,
+                                   void* stream, crt_layer** out) {
+  return prepare_impl(desc, w, ldw, bias, rank, nranks, (cudaStream_t)stream, out);
+}
+
+crt_status crt_layer_destroy(crt_layer* L) {
+  if (!L) return CRT_OK;
+  cudaFree(L->codes);
+  cudaFree(L->s32);
+  cudaFree(L->s64);
+  cudaFree(L->bias);
+  crt::k3_free_weights(&L->tiles);
+  delete L;
+  return CRT_OK;
+}
+
+crt_status crt_layer_info(const crt_layer* L, crt_layer_desc* out) {
+  if (!L || !out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
+  *out = L->desc;
+  return CRT_OK;
+}
+
+crt_status crt_layer_export(const crt_layer* L, uint8_t* codes, int64_t ld_codes, float* s32,
+                            double* s64, void* stream) {
+  if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t N = L->desc.out_features, K = L->desc.in_features;
+  const int64_t row = L->desc.bits_w == 4 ? (K + 1) / 2 : K;
+  cudaError_t e = cudaSuccess;
+  if (codes && N && row) {
+    if (ld_codes < row) return fail(CRT_ERR_SHAPE, "ld_codes too small");
+    e = cudaMemcpy2DAsync(codes, ld_codes, L->codes, L->ldc, row, N, cudaMemcpyDeviceToDevice, st);
+  }
+  if (e == cudaSuccess && s32 && N) e = cudaMemcpyAsync(s32, L->s32, 4 * N, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && s64 && N) e = cudaMemcpyAsync(s64, L->s64, 8 * N, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "layer export");
+  return CRT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3 + forward
+// ---------------------------------------------------------------------------
+crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                          int32_t bits_a, const crt_layer* L, int64_t M, int32_t out_kind,
+                          void* y, int64_t ldy, void* stream) {
+  if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
+  if (bits_a != 4 && bits_a != 8) return fail(CRT_ERR_INVALID_VALUE, "activation bits must be 4 or 8");
+  if (out_kind < CRT_OUT_BF16 || out_kind > CRT_OUT_I32_ACC)
+    return fail(CRT_ERR_INVALID_VALUE, "bad out_kind");
+  const int64_t N = L->desc.out_features, K = L->desc.in_features;
+  // int_gemm capacity precheck (pipeline.cpp:184-192)
+  const int64_t qa = (1 << (bits_a - 1)) - 1, qw = (1 << (L->desc.bits_w - 1)) - 1;
+  if (qa * qw * K > 2147483647LL)
+    return fail(CRT_ERR_CAPACITY, "int_gemm: " + std::to_string(K) +
+                                      "-deep accumulation can overflow int32");
+  if (bits_a != L->desc.bits_w)
+    return fail(CRT_ERR_UNSUPPORTED, "mixed activation/weight bit widths are not built");
+  if (M < 0) return fail(CRT_ERR_SHAPE, "negative M");
+  if (M == 0 || N == 0) return CRT_OK;
+  if (ldy < N) return fail(CRT_ERR_SHAPE, "ldy < N");
+  int64_t launches = 0;
+  crt::K3Args a{};
+  a.a_codes = a_codes;
+  a.lda = lda;
+  a.a_scales = a_scales;
+  a.w = L->tiles;
+  a.w_scales = L->s32;
+  a.bias = L->bias;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.bits = bits_a;
+  a.out_kind = out_kind;
+  a.y = y;
+  a.ldy = ldy;
+  cudaError_t e = crt::k3_launch(a, (cudaStream_t)stream, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess) return cuda_fail(e, "quant_gemm launch");
+  return CRT_OK;
+}
+
+crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** out) {
+  if (!out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
+  if (max_m < 0 || max_k < 0) return fail(CRT_ERR_SHAPE, "negative workspace size");
+  crt_workspace* w = new crt_workspace();
+  w->max_m = max_m;
+  w->max_k = max_k;
+  const int64_t ld = (max_k + 15) / 16 * 16;  // room for int8 codes too
+  cudaError_t e = cudaMalloc(&w->codes, (size_t)ld * (max_m ? max_m : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&w->s32, 4 * (size_t)(max_m ? max_m : 1));
+  if (e != cudaSuccess) {
+    cudaFree(w->codes);
+    delete w;
+    return cuda_fail(e, "workspace alloc");
+  }
+  *out = w;
+  return CRT_OK;
+}
+
+crt_status crt_workspace_destroy(crt_workspace* w) {
+  if (!w) return CRT_OK;
+  cudaFree(w->codes);
+  cudaFree(w->s32);
+  delete w;
+  return CRT_OK;
+}
+
+crt_status crt_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64_t M, int64_t ldx,
+                       int32_t bits_a, int32_t out_kind, void* y, int64_t ldy, crt_workspace* ws,
+                       void* stream) {
+  if (!L || !ws) return fail(CRT_ERR_INVALID_VALUE, "null layer / workspace");
+  const int64_t K = L->desc.in_features;
+  if (bits_a != 4 && bits_a != 8)  // pipeline.cpp:213-215
+    return fail(CRT_ERR_INVALID_VALUE, "forward: activation bits must be 4 or 8");
+  if (M > ws->max_m || K > ws->max_k) return fail(CRT_ERR_SHAPE, "workspace too small");
+  const int64_t ldc = bits_a == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
+  crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, bits_a, ws->codes, ldc, ws->s32,
+                        nullptr, (cudaStream_t)stream);
+  if (s != CRT_OK) return s;
+  return crt_quant_gemm(ws->codes, ldc, ws->s32, bits_a, L, M, out_kind, y, ldy, stream);
+}
+
+crt_status crt_forward_host(const crt_layer* L, const void* x_host, int32_t x_dtype, int64_t M,
+                            int32_t bits_a, int32_t out_kind, void* y_host, void* x_dev,
+                            void* y_dev, crt_workspace* ws, void* stream) {
+  if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = L->desc.in_features, N = L->desc.out_features;
+  const size_t xbytes = (size_t)M * K * (x_dtype == CRT_DTYPE_F32 ? 4 : 2);
+  const size_t ybytes = (size_t)M * N * (out_kind == CRT_OUT_BF16 ? 2 : 4);
+  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, xbytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "h2d");
+  crt_status s = crt_forward(L, x_dev, x_dtype, M, K, bits_a, out_kind, y_dev, N, ws, stream);
+  if (s != CRT_OK) return s;
+  e = cudaMemcpyAsync(y_host, y_dev, ybytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "d2h");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "sync");
+  return CRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// k1_rotate_quant.h -- host interface of K1 (rotate + quantize + pack).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace crt {
+
+struct K1Args {
+  const void* x;      // M x K (row stride ldx elements), bf16 or f32
+  int64_t ldx;
+  int64_t M;
+  int64_t K;
+  int64_t group;      // resolved group size (K for global); 1 for kind none
+  int64_t rot_cols;   // columns covered by whole groups (identity tail beyond)
+  int32_t kind;       // kRotNone / kRotSylvester / kRotRegular
+  int32_t team_warps; // filled by the plan
+  uint8_t* codes;     // M rows x ldc bytes
+  int64_t ldc;
+  float* s32;         // nullable
+  double* s64;        // nullable
+  int* err;           // device error word
+};
+
+struct K1Plan {
+  bool fast;
+  int C;  // 16-element chunks per lane
+  int W;  // warps per row team
+};
+
+K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, int bits,
+               const void* x, int64_t ldx, const void* codes, int64_t ldc);
+
+cudaError_t launch_k1(const K1Args& a, const K1Plan& p, bool f32, int bits, cudaStream_t st,
+                      int64_t* launches);
+
+}  // namespace crt
