@@ -30,7 +30,6 @@ namespace crt {
 namespace {
 
 constexpr uint32_t kMagic23 = 0x4B400000u;  // 1.5 * 2^23 : ulp 1
-constexpr uint32_t kMagic27 = 0x4D400000u;  // 1.5 * 2^27 : ulp 16
 
 template <bool F32>
 __device__ __forceinline__ double load_x(const void* row, int64_t j) {
@@ -293,6 +292,7 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
             const int bit = __ffs(m) - 1;
             m &= m - 1;
             const int64_t chunk = ((int64_t)(2 * p + (bit >> 4)) * W + w) * 32 + lane;
+            if (chunk >= nchunks) continue;
             cmax = fmax(cmax, fabs(y_ref<F32>(xrow, chunk * 16 + (bit & 15), a.group,
                                               a.kind, a.rot_cols)));
           }
@@ -322,50 +322,39 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
     uint8_t* crow = a.codes + row * a.ldc;
     if (!slow_row) {
       // ---- certified quantisation --------------------------------------------
+      // t = C + rint(y*inv) with C = 1.5*2^23 (ulp 1): the code is the low
+      // byte of t's bit pattern; e = y*inv - rint(y*inv) certifies it.
       const float inv = __double2float_rn(rk / s);
       const float margin = (float)(B * (rk / s) * 1.05) +
                            (float)(QMAX + 4) * 1.1920928955078125e-7f + 1e-9f;
       const float thr = 0.5f - margin;
-      const float inv16 = inv * 16.f;
-      const float2 inv_e = make_float2(inv, inv);
-      const float2 c_e = make_float2(__uint_as_float(kMagic23), __uint_as_float(kMagic23));
-      const float2 inv_o = BITS == 4 ? make_float2(inv16, inv16) : inv_e;
-      const float2 c_o =
-          BITS == 4 ? make_float2(__uint_as_float(kMagic27), __uint_as_float(kMagic27)) : c_e;
-      const float thr_o = BITS == 4 ? thr * 16.f : thr;
+      const float2 iv = make_float2(inv, inv);
+      const float2 cc = make_float2(__uint_as_float(kMagic23), __uint_as_float(kMagic23));
       uint32_t fmask[P];
 
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         uint32_t tb[2][16];
-        float emax_e = 0.f, emax_o = 0.f;
+        float emax = 0.f;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool odd = (i & 1) != 0;
-          const float2 iv = odd ? inv_o : inv_e;
-          const float2 cc = odd ? c_o : c_e;
           const float2 t = f2_fma(v[p][i], iv, cc);                  // C + rint(y*inv)
           const float2 nr = f2_fma(t, make_float2(-1.f, -1.f), cc);  // -rint(y*inv), exact
           const float2 e = f2_fma(v[p][i], iv, nr);                  // y*inv - rint
-          if (odd) emax_o = max3_abs(e.x, e.y, emax_o);
-          else emax_e = max3_abs(e.x, e.y, emax_e);
+          emax = max3_abs(e.x, e.y, emax);
           tb[0][i] = __float_as_uint(t.x);
           tb[1][i] = __float_as_uint(t.y);
         }
         uint32_t fm = 0;
-        if (!(emax_e <= thr) || !(emax_o <= thr_o)) {
+        if (!(emax <= thr)) {
           // rare: an element within the certified margin of a rounding
-          // boundary; remember which, fix after the store (below).
+          // boundary; remember which, decide it exactly after the store.
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const bool odd = (i & 1) != 0;
-            const float iv = (odd && BITS == 4) ? inv16 : inv;
-            const float cb = __uint_as_float((odd && BITS == 4) ? kMagic27 : kMagic23);
-            const float th = (odd && BITS == 4) ? thr_o : thr;
-            const float ex = fmaf(v[p][i].x, iv, cb - __uint_as_float(tb[0][i]));
-            const float ey = fmaf(v[p][i].y, iv, cb - __uint_as_float(tb[1][i]));
-            fm |= (fabsf(ex) <= th ? 0u : 1u) << i;
-            fm |= (fabsf(ey) <= th ? 0u : 1u) << (16 + i);
+            const float ex = fmaf(v[p][i].x, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[0][i]));
+            const float ey = fmaf(v[p][i].y, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[1][i]));
+            fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
+            fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
           }
         }
         fmask[p] = fm;
@@ -377,13 +366,8 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
           if constexpr (BITS == 4) {
             uint32_t by[8];
 #pragma unroll
-            for (int b2 = 0; b2 < 8; ++b2) {
-              uint32_t r;  // (odd & 0xF0) | (even & 0x0F)
-              asm("lop3.b32 %0, %1, %2, 0xF0, 0xE4;"
-                  : "=r"(r)
-                  : "r"(tb[h][2 * b2 + 1]), "r"(tb[h][2 * b2]));
-              by[b2] = r;
-            }
+            for (int b2 = 0; b2 < 8; ++b2)  // low byte = (odd << 4) | (even & 0xF)
+              by[b2] = tb[h][2 * b2 + 1] * 16u + (tb[h][2 * b2] & 0xFu);
             uint2 out;
             out.x = __byte_perm(__byte_perm(by[0], by[1], 0x0040),
                                 __byte_perm(by[2], by[3], 0x0040), 0x5410);
