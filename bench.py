@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""bench.py -- W4A4 ConvLinear4bit forward at the FLUX.1-dev MLP shapes.
+
+Workload (BASELINE.json configs[1], the largest single-GPU config the metric
+is quoted on): one "step" is the FLUX.1-dev MLP pair through the
+ConvLinear4bit path, N0 = 16, W4A4:
+    fc1: x[4608, 3072]  -> K1 rotate+quant -> K3 GEMM vs W1[12288, 3072] -> y1 bf16
+    fc2: y1[4608,12288] -> K1 rotate+quant -> K3 GEMM vs W2[3072, 12288] -> y2 bf16
+value  = 2*M*N*K summed over both layers / device time of the step (TOPS),
+         inputs resident in HBM, L2 flushed (256 MiB write) between steps.
+e2e    = same metric through the public API with HOST buffers: pinned x ->
+         device, both layers, y2 -> pinned host, every step.
+N > 1  = independent replicas (batch-8 prompt sharding): every rank runs the
+         full step on its own prompt; no data-path collective ("weak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "W4A4 ConvLinear4bit TOPS at FLUX.1 shapes; rot+quant HBM GB/s; vs CPU ref"
+M_TOK, D_MODEL, D_FF, N0 = 4608, 3072, 12288, 16
+WORKLOAD = ("FLUX.1-dev MLP pair: fc1 M=4608,K=3072,N=12288 and fc2 M=4608,K=12288,N=3072, "
+            "N0=16, W4A4 (configs[1])")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n0", type=int, default=N0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+def layer_ops():
+    return 2 * M_TOK * D_FF * D_MODEL + 2 * M_TOK * D_MODEL * D_FF
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference's own implementation (oracle/_ref, compiled from the
+# unmodified reference sources) on a bounded row sample of the same workload.
+# Rows are independent (per-token scales), so a row sample is the same work
+# per row as the full step.
+# ---------------------------------------------------------------------------
+class CpuReference:
+    def __init__(self, threads: int, seed: int = 0):
+        os.environ["CONVROT_THREADS"] = str(threads)
+        import numpy as np
+        import oracle as O
+        self.O = O
+        self.np = np
+        self.kind = "reference" if O.ref_available() else "port"
+        self.threads = threads if self.kind == "reference" else 1
+        rng = np.random.default_rng(seed)
+        # bf16-representable synthetic data (same distribution as the GPU arm)
+        def bf16(a):
+            return O.from_bf16_bits(O.to_bf16_bits(a))
+        self.w1 = bf16(rng.standard_normal((D_FF, D_MODEL)))
+        self.w2 = bf16(rng.standard_normal((D_MODEL, D_FF)))
+        self.b1 = bf16(rng.standard_normal(D_FF))
+        self.b2 = bf16(rng.standard_normal(D_MODEL))
+        self.x_all = bf16(rng.standard_normal((4096, D_MODEL)))
+        if self.kind == "reference":
+            self.l1 = O.Ref.prepare_layer(self.w1, self.b1, O.ROT_REGULAR, N0)
+            self.l2 = O.Ref.prepare_layer(self.w2, self.b2, O.ROT_REGULAR, N0)
+        else:
+            self.l1 = O.prepare_layer(self.w1, O.ROT_REGULAR, N0)
+            self.l2 = O.prepare_layer(self.w2, O.ROT_REGULAR, N0)
+
+    def step(self, rows: int) -> float:
+        O = self.O
+        x = self.x_all[:rows]
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            y1 = O.Ref.forward_prepared(x, self.l1[0], self.l1[1], self.b1, O.ROT_REGULAR, N0)
+            O.Ref.forward_prepared(y1, self.l2[0], self.l2[1], self.b2, O.ROT_REGULAR, N0)
+        else:
+            y1 = O.forward(x, self.l1[0], self.l1[1], self.b1, O.ROT_REGULAR, N0)["values"]
+            O.forward(y1, self.l2[0], self.l2[1], self.b2, O.ROT_REGULAR, N0)
+        return time.perf_counter() - t0
+
+    def calibrate(self, target_s: float = 12.0, max_rows: int = 4096) -> int:
+        rows = 16
+        t = self.step(rows)
+        while t < target_s / 4 and rows < max_rows:
+            rows = min(max_rows, rows * 4)
+            t = self.step(rows)
+        rows = max(16, min(max_rows, int(rows * target_s / max(t, 1e-3)) // 16 * 16))
+        return rows
+
+    def tops(self, rows: int, seconds: float) -> float:
+        return 2.0 * rows * (D_FF * D_MODEL + D_MODEL * D_FF) / seconds / 1e12
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # N>1: rank 0 alone runs and prints
+    threads = os.cpu_count() or 1
+    ref = CpuReference(threads)
+    rows = ref.calibrate(target_s=6.0, max_rows=1024)
+    for _ in range(args.warmup):
+        ref.step(rows)
+    times = [ref.step(rows) for _ in range(args.steps)]
+    t = statistics.mean(times)
+    v = ref.tops(rows, t)
+    sample = (f"{rows} of {M_TOK} token rows through fc1+fc2 per step (rows are independent: "
+              f"per-token scales); CONVROT_THREADS={ref.threads}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TOPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int4", "data": "synthetic (seeded gaussian, bf16-representable)",
+        "config": {"workload": WORKLOAD, "rows_per_step": rows, "n0": N0},
+        "cpu_baseline": {"value": v, "unit": "TOPS", "cores": ref.threads, "kind": ref.kind,
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        def reader():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 7:
+                    self.rows.append(parts)
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return float("nan")
+        sm = [num(r[0]) for r in self.rows]
+        mx = [num(r[1]) for r in self.rows]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        busy = [s for s in sm if not math.isnan(s)]
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_03673_b200 as crt
+    from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec, _abi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _abi.load()
+
+    n0 = args.n0
+    spec = RotationSpec(RotationKind.regular, n0)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    gw = torch.Generator(device=dev).manual_seed(99)  # same weights on every rank
+    x = torch.randn(M_TOK, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
+    w1 = torch.randn(D_FF, D_MODEL, device=dev, generator=gw).to(torch.bfloat16)
+    w2 = torch.randn(D_MODEL, D_FF, device=dev, generator=gw).to(torch.bfloat16)
+    b1 = torch.randn(D_FF, device=dev, generator=gw)
+    b2 = torch.randn(D_MODEL, device=dev, generator=gw)
+    fc1 = crt.prepare_layer(w1, b1, spec, QuantSpec(4), "fc1")
+    fc2 = crt.prepare_layer(w2, b2, spec, QuantSpec(4), "fc2")
+    del w1, w2
+
+    # preallocated device buffers (no allocation in the timed region)
+    ld1 = (D_MODEL // 2 + 15) // 16 * 16
+    ld2 = (D_FF // 2 + 15) // 16 * 16
+    c1 = torch.empty(M_TOK, ld1, dtype=torch.uint8, device=dev)
+    c2 = torch.empty(M_TOK, ld2, dtype=torch.uint8, device=dev)
+    s1 = torch.empty(M_TOK, dtype=torch.float32, device=dev)
+    s2 = torch.empty(M_TOK, dtype=torch.float32, device=dev)
+    y1 = torch.empty(M_TOK, D_FF, dtype=torch.bfloat16, device=dev)
+    y2 = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    rc = spec.c()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+
+    def k1(xin, codes, sc, K, ld):
+        _abi.check(lib.crt_rotate_quant(P(xin), _abi.CRT_DTYPE_BF16, M_TOK, K, K, ctypes.byref(rc),
+                                        4, P(codes), ld, P(sc), None, sp))
+
+    def k3(codes, ld, sc, layer, y, N):
+        _abi.check(lib.crt_quant_gemm(P(codes), ld, P(sc), 4, layer.handle, M_TOK,
+                                      _abi.CRT_OUT_BF16, P(y), N, sp))
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def step(record):
+        if record:
+            ev[0].record(stream)
+        k1(x, c1, s1, D_MODEL, ld1)
+        if record:
+            ev[1].record(stream)
+        k3(c1, ld1, s1, fc1, y1, D_FF)
+        if record:
+            ev[2].record(stream)
+        k1(y1, c2, s2, D_FF, ld2)
+        if record:
+            ev[3].record(stream)
+        k3(c2, ld2, s2, fc2, y2, D_MODEL)
+        if record:
+            ev[4].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = crt.launch_count()
+    seg = {"k1_fc1": [], "k3_fc1": [], "k1_fc2": [], "k3_fc2": [], "step": []}
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush, outside the event bracket
+        step(True)
+        ev[4].synchronize()
+        seg["k1_fc1"].append(ev[0].elapsed_time(ev[1]))
+        seg["k3_fc1"].append(ev[1].elapsed_time(ev[2]))
+        seg["k1_fc2"].append(ev[2].elapsed_time(ev[3]))
+        seg["k3_fc2"].append(ev[3].elapsed_time(ev[4]))
+        seg["step"].append(ev[0].elapsed_time(ev[4]))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = crt.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.stop()
+
+    ms_step = statistics.mean(seg["step"])
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    ops = layer_ops()
+    value = world * ops / (ms_step * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (K3), measured live on the launching stream
+    k3_us = (statistics.mean(seg["k3_fc1"]) + statistics.mean(seg["k3_fc2"])) / 2 * 1e3
+    k3_ops_per_launch = 2 * M_TOK * D_FF * D_MODEL  # both launches do 2*4608*3072*12288
+    k3_tops = k3_ops_per_launch / (k3_us * 1e-6) / 1e12
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_burst = float(peaks.get("bf16_tflops", 1590.0))
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    int8_peak = 2.0 * bf16_burst  # tcgen05 kind::i8 runs at 2x the kind::f16 rate
+    k1_bytes = {"fc1": M_TOK * D_MODEL * 2.5 + 4 * M_TOK, "fc2": M_TOK * D_FF * 2.5 + 4 * M_TOK}
+    k1_gbs = {k: k1_bytes[k] / (statistics.mean(seg[f"k1_{k}"]) * 1e-3) / 1e9 for k in k1_bytes}
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "k3_traffic.json"))).get(
+            "bytes_per_launch")
+    except Exception:
+        pass
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        xh = x.cpu().pin_memory()
+        yh = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16).pin_memory()
+        ws = crt.Workspace(M_TOK, D_FF, dev)
+        def e2e_step():
+            xd = xh.to(dev, non_blocking=True)
+            h = crt.forward(xd, fc1, QuantSpec(4), out="bf16", y=y1, workspace=ws)
+            o = crt.forward(h, fc2, QuantSpec(4), out="bf16", y=y2, workspace=ws)
+            yh.copy_(o, non_blocking=True)
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(3, args.steps // 2)
+        times = []
+        for _ in range(n_e2e):
+            es.record(stream)
+            e2e_step()
+            ee.record(stream)
+            ee.synchronize()
+            times.append(es.elapsed_time(ee))
+        e_ms = statistics.mean(times)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * ops / (e_ms * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": xh.numel() * 2, "d2h_bytes_per_step": yh.numel() * 2,
+               "ms_per_step": e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        try:
+            ref = CpuReference(os.cpu_count() or 1)
+            rows = ref.calibrate(target_s=12.0, max_rows=2048)
+            t = ref.step(rows)
+            cpu = {"value": ref.tops(rows, t), "unit": "TOPS", "cores": ref.threads,
+                   "kind": ref.kind,
+                   "sample": f"{rows} of {M_TOK} token rows through fc1+fc2 (one timed pass, "
+                             f"{t:.1f} s; CONVROT_THREADS={ref.threads})"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "TOPS", "cores": 0, "kind": "unavailable",
+                   "sample": f"error: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int4",
+            "data": "synthetic (seeded gaussian bf16 activations, random-init weights)",
+            "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
+                       "n0": n0, "bits": "W4A4", "parallelism": f"replica x{world}" if world > 1 else "single",
+                       "l2": "flushed (256 MiB write) between steps, outside the timed events"},
+            "roofline": {"bound": "tensor", "kernel": "k3_ss_kernel<4> (W4A4 GEMM)",
+                         "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",
+                         "frac": k3_tops / int8_peak, "traffic": traffic,
+                         "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json); "
+                                      f"vs nominal 4500: {k3_tops / 4500:.3f}",
+                         "ops_per_launch": k3_ops_per_launch, "avg_launch_us": k3_us},
+            "k1_roofline": {"bound": "hbm", "achieved": k1_gbs["fc2"], "peak": hbm, "unit": "GB/s",
+                            "frac": k1_gbs["fc2"] / hbm, "fc1_gbs": k1_gbs["fc1"],
+                            "bytes_per_launch": k1_bytes},
+            "kernels_us": {k: statistics.mean(v) * 1e3 for k, v in seg.items()},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clocks.summary(), "wall_s_timed": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
