@@ -10,12 +10,13 @@ from ._abi import (CapacityError, CudaError, Error, FormatError, InvalidOrderErr
                    InvalidValueError, ShapeError, UnsupportedError, load)
 from .api import (PreparedLayer, QuantSpec, RotationKind, RotationSpec, Workspace,  # noqa: F401
                   forward, int_gemm, launch_count, packed_row_bytes, prepare_layer,
-                  prepare_layer_shard, quant_gemm, regular, rotate_quantize, sylvester)
+                  prepare_layer_shard, quant_gemm, regular, rotate_quantize,
+                  rotate_quantize_into, sylvester)
 
 __all__ = [
     "Error", "InvalidOrderError", "InvalidValueError", "ShapeError", "CapacityError",
     "FormatError", "CudaError", "UnsupportedError", "RotationKind", "RotationSpec", "QuantSpec",
-    "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "prepare_layer",
+    "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "rotate_quantize_into", "prepare_layer",
     "prepare_layer_shard", "forward", "quant_gemm", "int_gemm", "launch_count",
     "packed_row_bytes", "load",
 ]

@@ -130,6 +130,21 @@ def rotate_quantize(x: torch.Tensor, rotation: RotationSpec, aq: QuantSpec = Qua
     return (codes, s32, s64) if scales64 else (codes, s32)
 
 
+def rotate_quantize_into(x: torch.Tensor, rotation: RotationSpec, codes: torch.Tensor,
+                         scales: torch.Tensor, aq: QuantSpec = QuantSpec(4),
+                         scales64: Optional[torch.Tensor] = None) -> None:
+    """rotate_quantize into caller-owned buffers (no allocation, no sync):
+    codes uint8 [M, ld] with ld >= packed row bytes, scales fp32 [M]."""
+    _check_2d_cuda(x, "x")
+    M, K = x.shape
+    if codes.shape[0] < M or codes.stride(1) != 1 or scales.numel() < M:
+        raise ShapeError("rotate_quantize_into: output buffers too small")
+    rc = rotation.c()
+    check(_lib().crt_rotate_quant(_ptr(x), _dtype_code(x), M, K, x.stride(0), ctypes.byref(rc),
+                                  aq.bits, _ptr(codes), codes.stride(0), _ptr(scales),
+                                  _ptr(scales64), _stream(x)))
+
+
 # ---------------------------------------------------------------------------
 # K2: prepare_layer (pipeline.cpp:158-176)
 # ---------------------------------------------------------------------------

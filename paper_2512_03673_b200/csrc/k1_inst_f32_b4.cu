@@ -3,6 +3,6 @@
 #include "k1_kernels.cuh"
 
 namespace crt {
-template cudaError_t k1_dispatch<true, 4>(const K1Args&, int, int, cudaStream_t, int64_t*);
+template cudaError_t k1_dispatch<true, 4>(const K1Args&, int, cudaStream_t, int64_t*);
 template cudaError_t k1_exact_launch<true, 4>(const K1Args&, cudaStream_t);
 }  // namespace crt

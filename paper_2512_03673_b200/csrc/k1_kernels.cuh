@@ -31,14 +31,20 @@ namespace {
 
 constexpr uint32_t kMagic23 = 0x4B400000u;  // 1.5 * 2^23 : ulp 1
 
+// Plain (generic-address) loads: `row` may point to global memory or to the
+// shared-memory copy of the row.
+template <bool F32>
+__device__ __forceinline__ float load_xf(const void* row, int64_t j) {
+  if constexpr (F32) {
+    return reinterpret_cast<const float*>(row)[j];
+  } else {
+    const uint16_t b = reinterpret_cast<const unsigned short*>(row)[j];
+    return __uint_as_float((uint32_t)b << 16);
+  }
+}
 template <bool F32>
 __device__ __forceinline__ double load_x(const void* row, int64_t j) {
-  if constexpr (F32) {
-    return (double)__ldg(reinterpret_cast<const float*>(row) + j);
-  } else {
-    uint16_t b = __ldg(reinterpret_cast<const unsigned short*>(row) + j);
-    return (double)__uint_as_float((uint32_t)b << 16);
-  }
+  return (double)load_xf<F32>(row, j);
 }
 
 // The reference's rotated value for column j of one row: out[j] =
@@ -60,6 +66,82 @@ __device__ __forceinline__ double y_ref(const void* row, int64_t j, int64_t grou
     acc = __dadd_rn(acc, __dmul_rn(load_x<F32>(row, base + k), neg ? -r : r));
   }
   return acc;
+}
+
+// y_ref(j) evaluated by a whole warp (all 32 lanes call it with the same j).
+// Lanes sum disjoint terms of the group in double and the partial sums are
+// combined with shuffles.  The reference's sequential sum (ascending k,
+// products +-x*2^-L exact) has no rounding at all whenever
+//     log2(group) + (emax - emin) + mantissa_bits <= 53
+// over the nonzero inputs of the group (all terms are integer multiples of
+// the smallest one's ulp and bounded by group * 2^(emax+1)); then EVERY
+// summation order yields the same exact value and the warp sum is returned.
+// Otherwise (subnormal / non-finite inputs or a huge exponent span) all
+// lanes redo the reference's sequential loop.
+template <bool F32>
+__device__ __noinline__ double y_exact_warp(const void* row, int64_t j, int64_t group, int kind,
+                                            int64_t rot_cols) {
+  if (kind == kRotNone || j >= rot_cols) return load_x<F32>(row, j);
+  const int lane = threadIdx.x & 31;
+  const int64_t base = j / group * group;
+  const uint32_t jj = (uint32_t)(j - base);
+  double acc = 0.0;
+  int emin = 1 << 20, emax = -1;
+  int bad = 0;
+  for (int k = lane; k < group; k += 32) {
+    const float x = load_xf<F32>(row, base + k);
+    const int e = (int)((__float_as_uint(x) >> 23) & 0xFFu);
+    if (x != 0.f) {
+      bad |= (e == 0 || e == 255) ? 1 : 0;
+      emin = min(emin, e);
+      emax = max(emax, e);
+    }
+    const bool neg = kind == kRotRegular ? regular_negative((uint32_t)k, jj)
+                                         : sylvester_negative((uint32_t)k, jj);
+    acc += neg ? -(double)x : (double)x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int l2 = __ffsll(group) - 1;
+  const bool pow4 = kind == kRotRegular || (l2 % 2 == 0);  // 1/sqrt(group) exact
+  if (!bad && pow4 && (emax < 0 || l2 + (emax - emin) + (F32 ? 24 : 8) <= 53))
+    return acc * (1.0 / sqrt((double)group));
+  return y_ref<F32>(row, j, group, kind, rot_cols);
+}
+
+// y_ref(j) for a group that lies in the calling lane's own chunk (N0 <= 16),
+// evaluated by that lane alone, given the fp32 butterfly value y32 (the
+// unnormalised sum).  If every partial sum of the fp32 butterflies is exact
+// -- all inputs of the group are integer multiples of the smallest one's
+// ulp and the intermediates (at most 2*group*max|x|) need
+//     1 + log2(group) + (emax - emin) + mantissa_bits <= 24 bits --
+// then y32 * 2^-L IS the reference's (exact) double value.  Otherwise the
+// reference's sequential double loop (at most 16 terms) is run.
+template <bool F32>
+__device__ __noinline__ double y_exact_lane(const void* row, int64_t j, int64_t group, int kind,
+                                            int64_t rot_cols, float y32) {
+  if (kind == kRotNone || j >= rot_cols) return load_x<F32>(row, j);
+  const int64_t base = j / group * group;
+  int emin = 1 << 20, emax = -1;
+  bool bad = false;
+  for (int64_t k = 0; k < group; ++k) {
+    const float x = load_xf<F32>(row, base + k);
+    const int e = (int)((__float_as_uint(x) >> 23) & 0xFFu);
+    if (x != 0.f) {
+      bad |= (e == 0 || e == 255);
+      emin = min(emin, e);
+      emax = max(emax, e);
+    }
+  }
+  const int l2 = __ffsll(group) - 1;
+  if (!bad && kind == kRotRegular && (emax < 0 || 1 + l2 + (emax - emin) + (F32 ? 24 : 8) <= 24))
+    return (double)y32 * (1.0 / sqrt((double)group));
+  return y_ref<F32>(row, j, group, kind, rot_cols);
 }
 
 __device__ __forceinline__ int exact_code(double y, double s, int qmax) {
@@ -121,11 +203,11 @@ __device__ __forceinline__ double team_max_d(double v, TeamScratch* ts, int team
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void bfly4(float2& a, float2& b, float2& c, float2& d) {
   const float2 m2 = make_float2(-2.f, -2.f);
-  float2 s = f2_add(f2_add(f2_add(a, b), c), d);
-  float2 na = f2_fma(m2, d, s);
-  float2 nb = f2_fma(m2, c, s);
-  float2 nc = f2_fma(m2, b, s);
-  float2 nd = f2_fma(m2, a, s);
+  float2 s = __fadd2_rn(__fadd2_rn(__fadd2_rn(a, b), c), d);
+  float2 na = __ffma2_rn(m2, d, s);
+  float2 nb = __ffma2_rn(m2, c, s);
+  float2 nc = __ffma2_rn(m2, b, s);
+  float2 nd = __ffma2_rn(m2, a, s);
   a = na;
   b = nb;
   c = nc;
@@ -147,30 +229,296 @@ struct Stages {
   static constexpr int L = N0 == 1 ? 0 : N0 == 4 ? 1 : N0 == 16 ? 2 : N0 == 64 ? 3 : 4;
 };
 
+
+// ---------------------------------------------------------------------------
+// Per-pair helpers of the fast kernel.  A "pair" is two 16-element chunks
+// (2p*W + w)*32 + lane and ((2p+1)*W + w)*32 + lane held as 16 fp32x2
+// registers v[i] = (chunk0[i], chunk1[i]).
+// ---------------------------------------------------------------------------
+template <bool F32, bool SMEM, bool FULL = false>
+__device__ __forceinline__ void load_pair(float2 (&v)[16], const void* rowp, int64_t c0,
+                                          int64_t cstride, int64_t nchunks) {
+  constexpr int CB = F32 ? 64 : 32;  // input bytes per chunk
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0 + h * cstride;
+    uint32_t u[CB / 4];
+    if (!FULL) {
+#pragma unroll
+      for (int i = 0; i < CB / 4; ++i) u[i] = 0u;
+    }
+    if (FULL || chunk < nchunks) {
+      const char* src = reinterpret_cast<const char*>(rowp) + chunk * CB;
+      if constexpr (SMEM) {
+        const uint32_t sa = smem_u32(src);
+#pragma unroll
+        for (int j = 0; j < CB / 16; ++j) {
+          const uint4 t = ld_shared_v4(sa + j * 16);
+          u[4 * j] = t.x;
+          u[4 * j + 1] = t.y;
+          u[4 * j + 2] = t.z;
+          u[4 * j + 3] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CB / 32; ++j) {
+          uint32_t t[8];
+          ld_nc_v8(src + 32 * j, t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) u[8 * j + i] = t[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float f;
+      if constexpr (F32) f = __uint_as_float(u[i]);
+      else f = __uint_as_float((i & 1) ? (u[i >> 1] & 0xFFFF0000u) : (u[i >> 1] << 16));
+      if (h == 0) v[i].x = f;
+      else v[i].y = f;
+    }
+  }
+}
+
+// Unnormalised regular-Hadamard sums of the groups in a pair: radix-4
+// stages over the in-chunk digits in registers, outer digits across lanes.
+// Warp-uniform (the shuffles need every lane).
+template <int N0>
+__device__ __forceinline__ void rotate_pair(float2 (&v)[16]) {
+  if constexpr (N0 >= 4) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) bfly4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+  }
+  if constexpr (N0 >= 16) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bfly4(v[j], v[j + 4], v[j + 8], v[j + 12]);
+  }
+  if constexpr (N0 >= 64) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i].x = xlane4(v[i].x, 1);
+      v[i].y = xlane4(v[i].y, 1);
+    }
+  }
+  if constexpr (N0 >= 256) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i].x = xlane4(v[i].x, 4);
+      v[i].y = xlane4(v[i].y, 4);
+    }
+  }
+}
+
+__device__ __forceinline__ float pair_absmax(const float2 (&v)[16]) {
+  float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    m0 = max3_abs(v[i].x, v[i].y, m0);
+    m1 = max3_abs(v[i + 1].x, v[i + 1].y, m1);
+  }
+  return max_nan(m0, m1);
+}
+
+// ---- out-of-line cold paths (kept out of the hot loop) ---------------------
+
+// Exact re-decision of flagged elements: bit (h*16 + e) of `m` flags
+// element e of chunk c0 + h*cstride.  c0 is the calling lane's own chunk;
+// the whole warp participates.
+template <bool F32, int BITS>
+__device__ __noinline__ void k1_redecide(uint32_t m, const void* rowp, uint8_t* crow,
+                                         int64_t c0, int64_t cstride, int64_t nchunks, double s,
+                                         int64_t group, int kind, int64_t rot_cols) {
+  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
+    if (!bal) break;
+    const int src = __ffs(bal) - 1;
+    const int bit = __shfl_sync(0xffffffffu, __ffs(m) - 1, src);
+    const int i = bit & 15;
+    const int64_t chunk = __shfl_sync(0xffffffffu, c0, src) + (bit >> 4) * cstride;
+    int code = 0;
+    if (chunk < nchunks)
+      code = exact_code(y_exact_warp<F32>(rowp, chunk * 16 + i, group, kind, rot_cols), s, QMAX);
+    if (lane == src) {
+      m &= m - 1;
+      if (chunk < nchunks) {
+        if constexpr (BITS == 4) {
+          uint8_t* bp = crow + chunk * 8 + (i >> 1);
+          const uint8_t old = *bp;
+          *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
+                        : (uint8_t)((old & 0xF0) | (code & 0x0F));
+        } else {
+          crow[chunk * 16 + i] = (uint8_t)code;
+        }
+      }
+    }
+  }
+}
+
+// Exact row maximum over the candidates |y32| >= thr of every lane that
+// has one.  A lane's candidates lie in its best pair `bp` unless its
+// second-best pair maximum also reaches thr (then all pairs are scanned).
+// Pairs are recomputed from the row copy; the exact values come from
+// y_exact_warp.  Whole warp participates.
+template <int N0, bool F32, bool SMEM>
+__device__ __noinline__ double k1_candidates_max(const void* rowp, int P, int W, int w,
+                                                 int64_t nchunks, bool has, int bp, bool all,
+                                                 float thr, int64_t group, int kind,
+                                                 int64_t rot_cols) {
+  const int lane = threadIdx.x & 31;
+  double cmax = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const bool need = has && (all || p == bp);
+    if (!__any_sync(0xffffffffu, need)) continue;
+    const int64_t c0 = ((int64_t)(2 * p) * W + w) * 32 + lane;
+    float2 v[16];
+    load_pair<F32, SMEM>(v, rowp, c0, (int64_t)W * 32, nchunks);
+    rotate_pair<N0>(v);
+    uint32_t m = 0;
+    if (need) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        m |= (fabsf(v[i].x) >= thr ? 1u : 0u) << i;
+        m |= (fabsf(v[i].y) >= thr ? 1u : 0u) << (16 + i);
+      }
+    }
+    for (;;) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
+      if (!bal) break;
+      const int src = __ffs(bal) - 1;
+      const int bit = __shfl_sync(0xffffffffu, __ffs(m) - 1, src);
+      const int64_t chunk = __shfl_sync(0xffffffffu, c0, src) + (bit >> 4) * (int64_t)W * 32;
+      double y = 0.0;
+      if (chunk < nchunks)
+        y = y_exact_warp<F32>(rowp, chunk * 16 + (bit & 15), group, kind, rot_cols);
+      if (lane == src) {
+        cmax = fmax(cmax, fabs(y));
+        m &= m - 1;
+      }
+    }
+  }
+  return cmax;
+}
+
+// Rows the fp32 path cannot certify (non-finite input, fp32 overflow):
+// the reference's max and codes element by element.
+template <bool F32>
+__device__ __noinline__ double k1_slow_row_amax(const void* rowp, int C, int W, int w,
+                                                int64_t nchunks, int64_t group, int kind,
+                                                int64_t rot_cols) {
+  const int lane = threadIdx.x & 31;
+  double m = 0.0;
+  bool bad = false;
+  for (int c = 0; c < C; ++c) {
+    const int64_t chunk = ((int64_t)c * W + w) * 32 + lane;
+    if (chunk >= nchunks) continue;
+    for (int i = 0; i < 16; ++i) {
+      const double yr = y_ref<F32>(rowp, chunk * 16 + i, group, kind, rot_cols);
+      if (!isfinite(yr)) bad = true;
+      m = fmax(m, fabs(yr));
+    }
+  }
+  return bad ? INFINITY : m;
+}
+
+template <bool F32, int BITS>
+__device__ __noinline__ void k1_slow_row_codes(const void* rowp, uint8_t* crow, int C, int W,
+                                               int w, int64_t nchunks, bool invalid, double s,
+                                               int64_t group, int kind, int64_t rot_cols) {
+  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < C; ++c) {
+    const int64_t chunk = ((int64_t)c * W + w) * 32 + lane;
+    if (chunk >= nchunks) continue;
+    for (int i = 0; i < 16; i += 2) {
+      int c0 = 0, c1 = 0;
+      if (!invalid) {
+        c0 = exact_code(y_ref<F32>(rowp, chunk * 16 + i, group, kind, rot_cols), s, QMAX);
+        c1 = exact_code(y_ref<F32>(rowp, chunk * 16 + i + 1, group, kind, rot_cols), s, QMAX);
+      }
+      if constexpr (BITS == 4) {
+        crow[chunk * 8 + i / 2] = (uint8_t)((c0 & 0x0F) | ((c1 & 0x0F) << 4));
+      } else {
+        crow[chunk * 16 + i] = (uint8_t)c0;
+        crow[chunk * 16 + i + 1] = (uint8_t)c1;
+      }
+    }
+  }
+}
+
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Fast kernel.
+//
+// Layout.  A team of W warps owns one row at a time; lane `lane` of warp w
+// handles the chunk pairs p < P = C/2 (chunks (2p*W + w)*32 + lane and
+// ((2p+1)*W + w)*32 + lane, 16 elements each).  A group of N0 <= 256
+// elements is N0/16 consecutive chunks = consecutive lanes, so in-chunk
+// radix-4 digits are in-register butterflies and outer digits are lane
+// shuffles.  C is a runtime value: the pair loop is rolled, so the hot loop
+// is small (instruction cache) and registers stay at one pair.
+//
+// Streaming.  Each team streams its rows through a ring of `stages`
+// shared-memory row buffers filled by 1-D bulk async copies (TMA engine,
+// cp.async.bulk, L2 evict-first) completing on one mbarrier per stage: HBM
+// reads of the next rows are in flight while the current row is processed.
+// Two passes read the row copy: pass 1 rotates and reduces the row absmax,
+// pass 2 rotates again and quantises / packs / stores (recomputing the
+// butterflies is cheaper than holding the row in registers).  !BULK reads
+// global memory directly (pass 2 then hits L1/L2).
+//
+// Certified rounding: see the file header and DESIGN.md.
+// ---------------------------------------------------------------------------
+constexpr int kK1MaxTeams = 8;
+constexpr int kK1MaxStages = 4;
+constexpr int kK1Threads = 256;
+constexpr int kK1MinBlocks = 3;  // rolled kernel: <= 85 registers, 24 warps per SM
 
-// ---------------------------------------------------------------------------
-// Fast kernel.  A team of W warps owns one row at a time; lane `lane` of
-// warp w holds chunks (c*W + w)*32 + lane, c < C, of 16 consecutive
-// elements each (C even; chunk pairs live in fp32x2 registers).  Groups of
-// N0 <= 256 elements are N0/16 consecutive chunks = consecutive lanes.
-// ---------------------------------------------------------------------------
-template <int C, int N0, bool F32, int BITS>
-__global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1Args a) {
-  constexpr int P = C / 2;
+template <int N0, bool F32, int BITS, bool BULK>
+__global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) {
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 4 ? 7 : 127;
   __shared__ TeamScratch ts;
+  __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
+  extern __shared__ __align__(128) uint8_t k1_ring[];
 
   const int W = a.team_warps;
+  const int P = a.chunks / 2;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int team = warp / W;
   const int w = warp - team * W;
   const int teams = blockDim.x / (32 * W);
   const int64_t nchunks = a.K / 16;
+  const int64_t cstride = (int64_t)W * 32;
   const int esz = F32 ? 4 : 2;
+  const int S = a.stages;
+  const uint32_t row_bytes = (uint32_t)(a.K * esz);
+  const bool leader = (w == 0 && lane == 0);
+  const int64_t row0 = (int64_t)blockIdx.x * teams + team;
+  const int64_t row_step = (int64_t)gridDim.x * teams;
+  uint8_t* ring = k1_ring + (size_t)team * S * row_bytes;
+
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) {
+      for (int t = 0; t < teams; ++t)
+        for (int s = 0; s < S; ++s) mbar_init(&full_bar[t][s], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (leader) {
+      for (int s = 0; s < S; ++s) {
+        const int64_t r = row0 + (int64_t)s * row_step;
+        if (r >= a.M) break;
+        mbar_arrive_expect_tx(&full_bar[team][s], row_bytes);
+        bulk_g2s(ring + (size_t)s * row_bytes,
+                 reinterpret_cast<const char*>(a.x) + r * a.ldx * esz, row_bytes,
+                 &full_bar[team][s]);
+      }
+    }
+  }
 
   // normalisation 2^-k = 1/sqrt(N0) (exact), and the certified bound factor
   const double rk = N0 == 1 ? 1.0 : 1.0 / sqrt((double)N0);
@@ -179,141 +527,57 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
                                   : (6.0 * L * sqrtn) * 5.9604644775390625e-8 +
                                         (double)N0 * sqrtn * 2.220446049250313e-16;
 
-  for (int64_t row = (int64_t)blockIdx.x * teams + team; row < a.M;
-       row += (int64_t)gridDim.x * teams) {
-    const char* xrow = reinterpret_cast<const char*>(a.x) + row * a.ldx * esz;
+  int it = 0;
+  for (int64_t row = row0; row < a.M; row += row_step, ++it) {
+    const int stage = BULK ? it % S : 0;
+    if constexpr (BULK) mbar_wait(&full_bar[team][stage], (uint32_t)((it / S) & 1));
+    const void* rowp =
+        BULK ? static_cast<const void*>(ring + (size_t)stage * row_bytes)
+             : static_cast<const void*>(reinterpret_cast<const char*>(a.x) + row * a.ldx * esz);
 
-    // ---- load + convert -------------------------------------------------
-    float2 v[P][16];
-#pragma unroll
+    // ---- pass 1: rotate, row absmax (NaN-propagating), best / 2nd pair ----
+    float lmax = 0.f, lmax_nan = 0.f, m2 = 0.f;
+    int bp = 0;
+#pragma unroll 1
     for (int p = 0; p < P; ++p) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t chunk = ((int64_t)(2 * p + h) * W + w) * 32 + lane;
-        float f[16];
-        if (chunk < nchunks) {
-          if constexpr (F32) {
-            uint32_t u0[8], u1[8];
-            ld_nc_v8(xrow + chunk * 64, u0);
-            ld_nc_v8(xrow + chunk * 64 + 32, u1);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              f[i] = __uint_as_float(u0[i]);
-              f[8 + i] = __uint_as_float(u1[i]);
-            }
-          } else {
-            uint32_t u[8];
-            ld_nc_v8(xrow + chunk * 32, u);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              f[2 * i] = __uint_as_float(u[i] << 16);
-              f[2 * i + 1] = __uint_as_float(u[i] & 0xFFFF0000u);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (h == 0) v[p][i].x = f[i];
-          else v[p][i].y = f[i];
-        }
+      float2 v[16];
+      load_pair<F32, BULK>(v, rowp, ((int64_t)(2 * p) * W + w) * 32 + lane, cstride, nchunks);
+      rotate_pair<N0>(v);
+      const float m = pair_absmax(v);
+      lmax_nan = max_nan(lmax_nan, m);
+      if (m > lmax) {
+        m2 = lmax;
+        lmax = m;
+        bp = p;
+      } else {
+        m2 = fmaxf(m2, m);
       }
     }
-
-    // ---- rotation (unnormalised sums of +-x) --------------------------------
-    if constexpr (N0 >= 4) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          bfly4(v[p][4 * g], v[p][4 * g + 1], v[p][4 * g + 2], v[p][4 * g + 3]);
-        if constexpr (N0 >= 16) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bfly4(v[p][j], v[p][j + 4], v[p][j + 8], v[p][j + 12]);
-        }
-      }
-    }
-    if constexpr (N0 >= 64) {
-#pragma unroll
-      for (int p = 0; p < P; ++p)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[p][i].x = xlane4(v[p][i].x, 1);
-          v[p][i].y = xlane4(v[p][i].y, 1);
-        }
-    }
-    if constexpr (N0 >= 256) {
-#pragma unroll
-      for (int p = 0; p < P; ++p)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          v[p][i].x = xlane4(v[p][i].x, 4);
-          v[p][i].y = xlane4(v[p][i].y, 4);
-        }
-    }
-
-    // ---- row absmax (NaN-propagating) ---------------------------------------
-    float lmax = 0.f;
-#pragma unroll
-    for (int p = 0; p < P; ++p)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) lmax = max3_abs(v[p][i].x, v[p][i].y, lmax);
-    const float A32 = team_max_nan(lmax, &ts, team, w, W);
+    const float A32 = team_max_nan(lmax_nan, &ts, team, w, W);
 
     // pathological rows (non-finite input, fp32 overflow) go the exact way
     const bool slow_row = !(A32 <= 3.0e38f);
     const double B = slow_row ? 0.0 : bound_rel * (double)A32 * 1.01;
     double amax_ref = 0.0;
     if (!slow_row) {
-      // candidates for the exact row max: |y32| >= A32 - 2B
-      const float thr = (float)((double)A32 - 2.0 * B) * (1.0f - 1e-6f);
-      double cmax = 0.0;
-      if (lmax >= thr) {
-        uint32_t cm[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          uint32_t m = 0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            m |= (fabsf(v[p][i].x) >= thr ? 1u : 0u) << i;
-            m |= (fabsf(v[p][i].y) >= thr ? 1u : 0u) << (16 + i);
-          }
-          cm[p] = m;
-        }
-#pragma unroll 1
-        for (int p = 0; p < P; ++p) {
-          uint32_t m = 0;
-#pragma unroll
-          for (int q = 0; q < P; ++q)
-            if (q == p) m = cm[q];
-          while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1;
-            const int64_t chunk = ((int64_t)(2 * p + (bit >> 4)) * W + w) * 32 + lane;
-            if (chunk >= nchunks) continue;
-            cmax = fmax(cmax, fabs(y_ref<F32>(xrow, chunk * 16 + (bit & 15), a.group,
-                                              a.kind, a.rot_cols)));
-          }
-        }
+      if (N0 == 1 || A32 == 0.f) {
+        // no rotation: y32 == x exactly; all-zero fp32 sums <=> all-zero row
+        amax_ref = (double)A32;
+      } else {
+        // candidates for the exact row max: |y32| >= A32 - 2B,
+        // each settled by the warp-cooperative exact evaluation
+        const float thr = (float)((double)A32 - 2.0 * B) * (1.0f - 1e-6f);
+        const bool has = lmax >= thr;
+        double cmax = 0.0;
+        if (__any_sync(0xffffffffu, has))
+          cmax = k1_candidates_max<N0, F32, BULK>(rowp, P, W, w, nchunks, has, bp, m2 >= thr,
+                                                  thr, a.group, a.kind, a.rot_cols);
+        amax_ref = team_max_d(cmax, &ts, team, w, W);
       }
-      amax_ref = team_max_d(cmax, &ts, team, w, W);
     } else {
-      double m = 0.0;
-      bool bad = false;
-#pragma unroll 1
-      for (int c = 0; c < C; ++c) {
-        const int64_t chunk = ((int64_t)c * W + w) * 32 + lane;
-        if (chunk >= nchunks) continue;
-#pragma unroll 1
-        for (int i = 0; i < 16; ++i) {
-          double yr = y_ref<F32>(xrow, chunk * 16 + i, a.group, a.kind, a.rot_cols);
-          if (!isfinite(yr)) bad = true;
-          m = fmax(m, fabs(yr));
-        }
-      }
-      amax_ref = team_max_d(bad ? INFINITY : m, &ts, team, w, W);
+      amax_ref = team_max_d(k1_slow_row_amax<F32>(rowp, a.chunks, W, w, nchunks, a.group,
+                                                  a.kind, a.rot_cols),
+                            &ts, team, w, W);
     }
     const bool invalid = !isfinite(amax_ref);
     const double s = invalid ? 1.0 : (amax_ref == 0.0 ? 1.0 : amax_ref / (double)QMAX);
@@ -321,47 +585,38 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
 
     uint8_t* crow = a.codes + row * a.ldc;
     if (!slow_row) {
-      // ---- certified quantisation --------------------------------------------
-      // t = C + rint(y*inv) with C = 1.5*2^23 (ulp 1): the code is the low
-      // byte of t's bit pattern; e = y*inv - rint(y*inv) certifies it.
-      const float inv = __double2float_rn(rk / s);
-      const float margin = (float)(B * (rk / s) * 1.05) +
+      // ---- pass 2: certified quantisation + pack + store ---------------------
+      // t = M + rint(y*inv) with M = 1.5*2^23 (ulp 1): the low byte of its
+      // bit pattern is the two's-complement code; e = y*inv - rint(y*inv)
+      // certifies the decision against the reference's double rint(y/s).
+      const double invd = rk / s;
+      const float inv = __double2float_rn(invd);
+      const float margin = (float)(B * invd * 1.05) +
                            (float)(QMAX + 4) * 1.1920928955078125e-7f + 1e-9f;
       const float thr = 0.5f - margin;
       const float2 iv = make_float2(inv, inv);
       const float2 cc = make_float2(__uint_as_float(kMagic23), __uint_as_float(kMagic23));
-      uint32_t fmask[P];
-
-#pragma unroll
+#pragma unroll 1
       for (int p = 0; p < P; ++p) {
+        const int64_t c0 = ((int64_t)(2 * p) * W + w) * 32 + lane;
+        float2 v[16];
+        load_pair<F32, BULK>(v, rowp, c0, cstride, nchunks);
+        rotate_pair<N0>(v);
         uint32_t tb[2][16];
-        float emax = 0.f;
+        float em0 = 0.f, em1 = 0.f;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float2 t = f2_fma(v[p][i], iv, cc);                  // C + rint(y*inv)
-          const float2 nr = f2_fma(t, make_float2(-1.f, -1.f), cc);  // -rint(y*inv), exact
-          const float2 e = f2_fma(v[p][i], iv, nr);                  // y*inv - rint
-          emax = max3_abs(e.x, e.y, emax);
+          const float2 t = __ffma2_rn(v[i], iv, cc);                      // M + rint(y*inv)
+          const float2 nr = __ffma2_rn(t, make_float2(-1.f, -1.f), cc);   // -rint(y*inv)
+          const float2 e = __ffma2_rn(v[i], iv, nr);                      // y*inv - rint
+          if (i & 1) em1 = max3_abs(e.x, e.y, em1);
+          else em0 = max3_abs(e.x, e.y, em0);
           tb[0][i] = __float_as_uint(t.x);
           tb[1][i] = __float_as_uint(t.y);
         }
-        uint32_t fm = 0;
-        if (!(emax <= thr)) {
-          // rare: an element within the certified margin of a rounding
-          // boundary; remember which, decide it exactly after the store.
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float ex = fmaf(v[p][i].x, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[0][i]));
-            const float ey = fmaf(v[p][i].y, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[1][i]));
-            fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
-            fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
-          }
-        }
-        fmask[p] = fm;
-        // ---- pack + store ------------------------------------------------------
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int64_t chunk = ((int64_t)(2 * p + h) * W + w) * 32 + lane;
+          const int64_t chunk = c0 + h * cstride;
           if (chunk >= nchunks) continue;
           if constexpr (BITS == 4) {
             uint32_t by[8];
@@ -381,61 +636,403 @@ __global__ void __launch_bounds__(256, C <= 2 ? 3 : (C <= 4 ? 2 : 1)) k1_fast(K1
               wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                                    __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
                                    0x5410);
-            *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+            *reinterpret_cast<uint4*>(crow + chunk * 16) =
+                make_uint4(wds[0], wds[1], wds[2], wds[3]);
           }
         }
-      }
-      // ---- exact decisions for the flagged elements (same thread re-writes
-      // the byte it stored above; program order makes that safe) ---------------
-#pragma unroll 1
-      for (int p = 0; p < P; ++p) {
-        uint32_t m = 0;
+        // rare: an element of this pair within the certified margin of a
+        // rounding boundary -> all 32 re-decided exactly (owner lane
+        // re-writes the bytes it just stored; program order makes it safe)
+        uint32_t fm = 0u;
+        if (!(max_nan(em0, em1) <= thr)) {
+          // rare: some element lies within the certified margin of a
+          // rounding boundary (exact ties y/s = k + 1/2 are common with
+          // discrete bf16 data); find which
 #pragma unroll
-        for (int q = 0; q < P; ++q)
-          if (q == p) m = fmask[q];
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          m &= m - 1;
-          const int i = bit & 15;
-          const int64_t chunk = ((int64_t)(2 * p + (bit >> 4)) * W + w) * 32 + lane;
-          if (chunk >= nchunks) continue;
-          const int code = exact_code(
-              y_ref<F32>(xrow, chunk * 16 + i, a.group, a.kind, a.rot_cols), s, QMAX);
-          if constexpr (BITS == 4) {
-            uint8_t* bp = crow + chunk * 8 + (i >> 1);
-            const uint8_t old = *bp;
-            *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
-                          : (uint8_t)((old & 0xF0) | (code & 0x0F));
-          } else {
-            crow[chunk * 16 + i] = (uint8_t)code;
+          for (int i = 0; i < 16; ++i) {
+            const float ex = fmaf(v[i].x, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[0][i]));
+            const float ey = fmaf(v[i].y, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[1][i]));
+            fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
+            fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
           }
         }
+        if (__any_sync(0xffffffffu, fm != 0u))
+          k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
+                                 a.rot_cols);
       }
     } else {
-      // slow row: exact codes for every element
-#pragma unroll 1
-      for (int c = 0; c < C; ++c) {
-        const int64_t chunk = ((int64_t)c * W + w) * 32 + lane;
-        if (chunk >= nchunks) continue;
-#pragma unroll 1
-        for (int i = 0; i < 16; i += 2) {
-          int c0 = 0, c1 = 0;
-          if (!invalid) {
-            c0 = exact_code(y_ref<F32>(xrow, chunk * 16 + i, a.group, a.kind, a.rot_cols), s, QMAX);
-            c1 = exact_code(y_ref<F32>(xrow, chunk * 16 + i + 1, a.group, a.kind, a.rot_cols), s, QMAX);
-          }
-          if constexpr (BITS == 4) {
-            crow[chunk * 8 + i / 2] = (uint8_t)((c0 & 0x0F) | ((c1 & 0x0F) << 4));
-          } else {
-            crow[chunk * 16 + i] = (uint8_t)c0;
-            crow[chunk * 16 + i + 1] = (uint8_t)c1;
-          }
-        }
-      }
+      k1_slow_row_codes<F32, BITS>(rowp, crow, a.chunks, W, w, nchunks, invalid, s, a.group,
+                                   a.kind, a.rot_cols);
     }
     if (w == 0 && lane == 0) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
+    }
+    if constexpr (BULK) {
+      // every lane of the team is done with this stage (both passes and the
+      // exact re-evaluations): refill it with the row `stages` ahead.
+      if (W == 1) __syncwarp();
+      else named_bar_sync(1 + team, W * 32);
+      if (leader) {
+        const int64_t r = row + (int64_t)S * row_step;
+        if (r < a.M) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&full_bar[team][stage], row_bytes);
+          bulk_g2s(ring + (size_t)stage * row_bytes,
+                   reinterpret_cast<const char*>(a.x) + r * a.ldx * esz, row_bytes,
+                   &full_bar[team][stage]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single-pass fast kernel (K <= 24576): the row's C chunks per lane stay in
+// registers (fp32x2 pairs, fully unrolled), so each element is loaded once
+// from the shared-memory row copy, rotated once and quantised from
+// registers.  Per-row work (row absmax, exact max candidates, scale) is
+// amortised over 16*C elements per lane.  Layout / streaming / certified
+// rounding as in k1_rolled above.
+// ---------------------------------------------------------------------------
+constexpr int kK1FThreads = 192;  // 6 warps; two CTAs per SM at <= 170 registers
+constexpr int kK1FMinBlocks = 2;
+
+// Lane-local exact decisions (N0 <= 16): flagged bits (h*16 + i) of `m`
+// index the 32 fp32 sums vl[] of the calling lane's chunk pair.
+template <bool F32, int BITS>
+__device__ __noinline__ void k1_redecide_lane(uint32_t m, const float2* vl, const void* rowp,
+                                              uint8_t* crow, int64_t c0, int64_t cstride,
+                                              int64_t nchunks, double s, int64_t group, int kind,
+                                              int64_t rot_cols) {
+  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    const int i = bit & 15;
+    const int64_t chunk = c0 + (bit >> 4) * cstride;
+    if (chunk >= nchunks) continue;
+    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
+    const int code = exact_code(y_exact_lane<F32>(rowp, chunk * 16 + i, group, kind, rot_cols, y32),
+                                s, QMAX);
+    if constexpr (BITS == 4) {
+      uint8_t* bp = crow + chunk * 8 + (i >> 1);
+      const uint8_t old = *bp;
+      *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
+                    : (uint8_t)((old & 0xF0) | (code & 0x0F));
+    } else {
+      crow[chunk * 16 + i] = (uint8_t)code;
+    }
+  }
+}
+
+// Lane-local exact |y_ref| maximum over the lane's candidates (N0 <= 16).
+template <bool F32>
+__device__ __noinline__ double k1_cands_lane(uint32_t m, const float2* vl, const void* rowp,
+                                             int64_t c0, int64_t cstride, int64_t nchunks,
+                                             int64_t group, int kind, int64_t rot_cols) {
+  double cmax = 0.0;
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    const int i = bit & 15;
+    const int64_t chunk = c0 + (bit >> 4) * cstride;
+    if (chunk >= nchunks) continue;
+    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
+    cmax = fmax(cmax, fabs(y_exact_lane<F32>(rowp, chunk * 16 + i, group, kind, rot_cols, y32)));
+  }
+  return cmax;
+}
+
+// Warp-cooperative versions (N0 >= 64: a group spans lanes).
+template <bool F32>
+__device__ __noinline__ double k1_cands_warp(uint32_t m, const void* rowp, int64_t c0,
+                                             int64_t cstride, int64_t nchunks, int64_t group,
+                                             int kind, int64_t rot_cols) {
+  const int lane = threadIdx.x & 31;
+  double cmax = 0.0;
+  for (;;) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
+    if (!bal) break;
+    const int src = __ffs(bal) - 1;
+    const int bit = __shfl_sync(0xffffffffu, __ffs(m) - 1, src);
+    const int64_t chunk = __shfl_sync(0xffffffffu, c0, src) + (bit >> 4) * cstride;
+    double y = 0.0;
+    if (chunk < nchunks) y = y_exact_warp<F32>(rowp, chunk * 16 + (bit & 15), group, kind, rot_cols);
+    if (lane == src) {
+      cmax = fmax(cmax, fabs(y));
+      m &= m - 1;
+    }
+  }
+  return cmax;
+}
+
+template <int C, int N0, bool F32, int BITS, bool BULK, bool FULL>
+__global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) {
+  constexpr int P = C / 2;
+  constexpr int L = Stages<N0>::L;
+  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  __shared__ TeamScratch ts;
+  __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
+  extern __shared__ __align__(128) uint8_t k1_ring[];
+
+  const int W = a.team_warps;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int team = warp / W;
+  const int w = warp - team * W;
+  const int teams = blockDim.x / (32 * W);
+  const int64_t nchunks = a.K / 16;
+  const int64_t cstride = (int64_t)W * 32;
+  const int esz = F32 ? 4 : 2;
+  const int S = a.stages;
+  const uint32_t row_bytes = (uint32_t)(a.K * esz);
+  const bool leader = (w == 0 && lane == 0);
+  const int64_t row0 = (int64_t)blockIdx.x * teams + team;
+  const int64_t row_step = (int64_t)gridDim.x * teams;
+  uint8_t* ring = k1_ring + (size_t)team * S * row_bytes;
+
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) {
+      for (int t = 0; t < teams; ++t)
+        for (int s = 0; s < S; ++s) mbar_init(&full_bar[t][s], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (leader) {
+      for (int s = 0; s < S; ++s) {
+        const int64_t r = row0 + (int64_t)s * row_step;
+        if (r >= a.M) break;
+        mbar_arrive_expect_tx(&full_bar[team][s], row_bytes);
+        bulk_g2s(ring + (size_t)s * row_bytes,
+                 reinterpret_cast<const char*>(a.x) + r * a.ldx * esz, row_bytes,
+                 &full_bar[team][s]);
+      }
+    }
+  }
+
+  const double rk = N0 == 1 ? 1.0 : 1.0 / sqrt((double)N0);
+  const double sqrtn = N0 == 1 ? 1.0 : sqrt((double)N0);
+  const double bound_rel = L == 0 ? 0.0
+                                  : (6.0 * L * sqrtn) * 5.9604644775390625e-8 +
+                                        (double)N0 * sqrtn * 2.220446049250313e-16;
+
+  int it = 0;
+  for (int64_t row = row0; row < a.M; row += row_step, ++it) {
+    const int stage = BULK ? it % S : 0;
+    if constexpr (BULK) mbar_wait(&full_bar[team][stage], (uint32_t)((it / S) & 1));
+    const void* rowp =
+        BULK ? static_cast<const void*>(ring + (size_t)stage * row_bytes)
+             : static_cast<const void*>(reinterpret_cast<const char*>(a.x) + row * a.ldx * esz);
+
+    // ---- load + rotate (all pairs in registers) ----------------------------
+    float2 v[P][16];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      load_pair<F32, BULK, FULL>(v[p], rowp, ((int64_t)(2 * p) * W + w) * 32 + lane, cstride,
+                                 nchunks);
+      rotate_pair<N0>(v[p]);
+    }
+
+    // ---- row absmax (NaN-propagating) with per-quad sub-maxima -------------
+    float qmx[P][4];
+    float pmx[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float m0 = max3_abs(v[p][4 * q].x, v[p][4 * q].y, 0.f);
+        const float m1 = max3_abs(v[p][4 * q + 1].x, v[p][4 * q + 1].y, 0.f);
+        const float m2 = max3_abs(v[p][4 * q + 2].x, v[p][4 * q + 2].y, m0);
+        const float m3 = max3_abs(v[p][4 * q + 3].x, v[p][4 * q + 3].y, m1);
+        qmx[p][q] = max_nan(m2, m3);
+      }
+      pmx[p] = max_nan(max_nan(qmx[p][0], qmx[p][1]), max_nan(qmx[p][2], qmx[p][3]));
+    }
+    float lmax = pmx[0];
+#pragma unroll
+    for (int p = 1; p < P; ++p) lmax = max_nan(lmax, pmx[p]);
+    const float A32 = team_max_nan(lmax, &ts, team, w, W);
+
+    // pathological rows (non-finite input, fp32 overflow) go the exact way
+    const bool slow_row = !(A32 <= 3.0e38f);
+    const double B = slow_row ? 0.0 : bound_rel * (double)A32 * 1.01;
+    double amax_ref = 0.0;
+    if (!slow_row) {
+      if (N0 == 1 || A32 == 0.f) {
+        // no rotation: y32 == x exactly; all-zero fp32 sums <=> all-zero row
+        amax_ref = (double)A32;
+      } else {
+        // candidates for the exact row max: |y32| >= A32 - 2B
+        const float thr = (float)((double)A32 - 2.0 * B) * (1.0f - 1e-6f);
+        double cmax = 0.0;
+        if constexpr (N0 <= 16) {
+          if (lmax >= thr) {  // lane-local (divergent) scan of the quads
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+              uint32_t m = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (qmx[p][q] >= thr) {
+#pragma unroll
+                  for (int i = 4 * q; i < 4 * q + 4; ++i) {
+                    m |= (fabsf(v[p][i].x) >= thr ? 1u : 0u) << i;
+                    m |= (fabsf(v[p][i].y) >= thr ? 1u : 0u) << (16 + i);
+                  }
+                }
+              if (m) {
+                float2 vl[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) vl[i] = v[p][i];
+                cmax = fmax(cmax, k1_cands_lane<F32>(m, vl, rowp,
+                                                     ((int64_t)(2 * p) * W + w) * 32 + lane,
+                                                     cstride, nchunks, a.group, a.kind,
+                                                     a.rot_cols));
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            uint32_t m = 0;
+            if (lmax >= thr) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (qmx[p][q] >= thr) {
+#pragma unroll
+                  for (int i = 4 * q; i < 4 * q + 4; ++i) {
+                    m |= (fabsf(v[p][i].x) >= thr ? 1u : 0u) << i;
+                    m |= (fabsf(v[p][i].y) >= thr ? 1u : 0u) << (16 + i);
+                  }
+                }
+            }
+            if (__any_sync(0xffffffffu, m != 0))
+              cmax = fmax(cmax, k1_cands_warp<F32>(m, rowp, ((int64_t)(2 * p) * W + w) * 32 + lane,
+                                                   cstride, nchunks, a.group, a.kind,
+                                                   a.rot_cols));
+          }
+        }
+        amax_ref = team_max_d(cmax, &ts, team, w, W);
+      }
+    } else {
+      amax_ref = team_max_d(k1_slow_row_amax<F32>(rowp, C, W, w, nchunks, a.group, a.kind,
+                                                  a.rot_cols),
+                            &ts, team, w, W);
+    }
+    const bool invalid = !isfinite(amax_ref);
+    const double s = invalid ? 1.0 : (amax_ref == 0.0 ? 1.0 : amax_ref / (double)QMAX);
+    if (invalid && lane == 0 && w == 0) flag_invalid_value(a.err);
+
+    uint8_t* crow = a.codes + row * a.ldc;
+    if (!slow_row) {
+      // ---- certified quantisation + pack + store ------------------------------
+      // t = M + rint(y*inv) with M = 1.5*2^23 (ulp 1): the low byte of its
+      // bit pattern is the two's-complement code; e = y*inv - rint(y*inv)
+      // certifies the decision against the reference's double rint(y/s).
+      // inv = fl32(rk / fl32(s)) is within 2 ulp of rk/s: covered by the
+      // (QMAX + 4) ulp slack of the margin.
+      const float sf = (float)s;
+      const float inv = __fdiv_rn((float)rk, sf);
+      const float margin = (float)B * (inv * 1.05f) +
+                           (float)(QMAX + 4) * 1.1920928955078125e-7f + 1e-9f;
+      const float thr = 0.5f - margin;
+      // 4-bit codes use the biased magic M + 8, so the low nibble of t is
+      // code + 8 in [1, 15] with nothing above it: one IMAD packs a byte
+      // (odd*16 + even) in offset binary and one XOR 0x88888888 per word
+      // turns it into two's-complement nibbles.
+      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
+      const float2 iv = make_float2(inv, inv);
+      const float2 cc = make_float2(mg, mg);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int64_t c0 = ((int64_t)(2 * p) * W + w) * 32 + lane;
+        uint32_t tb[2][16];
+        float em[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 t = __ffma2_rn(v[p][i], iv, cc);                   // M + rint(y*inv)
+          const float2 nr = __ffma2_rn(t, make_float2(-1.f, -1.f), cc);   // -rint(y*inv)
+          const float2 e = __ffma2_rn(v[p][i], iv, nr);                   // y*inv - rint
+          em[i & 3] = max3_abs(e.x, e.y, em[i & 3]);
+          tb[0][i] = __float_as_uint(t.x);
+          tb[1][i] = __float_as_uint(t.y);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t chunk = c0 + h * cstride;
+          if (!FULL && chunk >= nchunks) continue;
+          if constexpr (BITS == 4) {
+            uint32_t by[8];
+#pragma unroll
+            for (int b2 = 0; b2 < 8; ++b2)  // low byte = 16*(odd+8) + (even+8)
+              by[b2] = tb[h][2 * b2 + 1] * 16u + tb[h][2 * b2];
+            uint2 out;
+            out.x = __byte_perm(__byte_perm(by[0], by[1], 0x0040),
+                                __byte_perm(by[2], by[3], 0x0040), 0x5410) ^ 0x88888888u;
+            out.y = __byte_perm(__byte_perm(by[4], by[5], 0x0040),
+                                __byte_perm(by[6], by[7], 0x0040), 0x5410) ^ 0x88888888u;
+            *reinterpret_cast<uint2*>(crow + chunk * 8) = out;
+          } else {
+            uint32_t wds[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
+                                   __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
+                                   0x5410);
+            *reinterpret_cast<uint4*>(crow + chunk * 16) =
+                make_uint4(wds[0], wds[1], wds[2], wds[3]);
+          }
+        }
+        // rare: elements within the certified margin of a rounding boundary
+        // (exact ties y/s = k + 1/2 are common with discrete bf16 data):
+        // decided exactly; the owner re-writes the bytes it just stored.
+        uint32_t fm = 0u;
+        if (!(max_nan(max_nan(em[0], em[1]), max_nan(em[2], em[3])) <= thr)) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float ex = fmaf(v[p][i].x, inv, mg - __uint_as_float(tb[0][i]));
+            const float ey = fmaf(v[p][i].y, inv, mg - __uint_as_float(tb[1][i]));
+            fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
+            fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
+          }
+        }
+        if constexpr (N0 <= 16) {
+          if (fm) {
+            float2 vl[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vl[i] = v[p][i];
+            k1_redecide_lane<F32, BITS>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
+                                        a.kind, a.rot_cols);
+          }
+        } else {
+          if (__any_sync(0xffffffffu, fm != 0u))
+            k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
+                                   a.rot_cols);
+        }
+      }
+    } else {
+      k1_slow_row_codes<F32, BITS>(rowp, crow, C, W, w, nchunks, invalid, s, a.group, a.kind,
+                                   a.rot_cols);
+    }
+    if (w == 0 && lane == 0) {
+      if (a.s32) a.s32[row] = (float)s;
+      if (a.s64) a.s64[row] = s;
+    }
+    if constexpr (BULK) {
+      // every lane of the team is done with this stage: refill it with the
+      // row `stages` ahead.
+      if (W == 1) __syncwarp();
+      else named_bar_sync(1 + team, W * 32);
+      if (leader) {
+        const int64_t r = row + (int64_t)S * row_step;
+        if (r < a.M) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&full_bar[team][stage], row_bytes);
+          bulk_g2s(ring + (size_t)stage * row_bytes,
+                   reinterpret_cast<const char*>(a.x) + r * a.ldx * esz, row_bytes,
+                   &full_bar[team][stage]);
+        }
+      }
     }
   }
 }
@@ -503,53 +1100,128 @@ __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
   }
 }
 
-template <int C, int N0, bool F32, int BITS>
-cudaError_t launch_fast(const K1Args& a, cudaStream_t st, int64_t* launches) {
-  auto kern = k1_fast<C, N0, F32, BITS>;
-  const int W = a.team_warps;
-  const int teams = W >= 8 ? 1 : 8 / W;  // 256-thread CTAs (W | 8) or one team
-  const int threads = teams * W * 32;
+template <int N0, bool F32, int BITS>
+cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  K1Args a = a0;
+  const int W = a.team_warps;
+  const size_t rb = (size_t)a.K * (F32 ? 4 : 2);
+  // Teams per CTA: fill the CTA, but never more teams than rows per SM.
+  int teams = kK1Threads / (W * 32);
+  teams = teams < 1 ? 1 : (teams > kK1MaxTeams ? kK1MaxTeams : teams);
+  const int64_t rows_per_sm = (a.M + num_sms - 1) / num_sms;
+  if (teams > rows_per_sm) teams = (int)(rows_per_sm < 1 ? 1 : rows_per_sm);
+  // Shared-memory row ring: ~216 KB per SM split over the CTAs that fit by
+  // registers (kK1MinBlocks); as many stages as fit, up to kK1MaxStages.
+  const size_t budget = (size_t)216 * 1024 / kK1MinBlocks;
+  int S = (int)(budget / ((size_t)teams * rb));
+  if (S > kK1MaxStages) S = kK1MaxStages;
+  const bool bulk = S >= 1 && ((uintptr_t)a.x % 16 == 0) && ((a.ldx * (F32 ? 4 : 2)) % 16 == 0);
+  a.stages = bulk ? S : 1;
+  const int threads = teams * W * 32;
+  const size_t smem = bulk ? (size_t)teams * S * rb : 0;
+  auto kern = bulk ? k1_rolled<N0, F32, BITS, true> : k1_rolled<N0, F32, BITS, false>;
+  if (bulk) {
+    static size_t smem_set = 0;  // per instantiation
+    if (smem > smem_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      // all of L1 as shared memory, or the SM holds a single CTA
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      smem_set = smem;
+    }
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
-  int64_t need = (a.M + teams - 1) / teams;
+  const int64_t need = (a.M + teams - 1) / teams;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, threads, 0, st>>>(a);
+  kern<<<(unsigned)grid, threads, smem, st>>>(a);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int C, bool F32, int BITS>
-cudaError_t dispatch_n0(const K1Args& a, int n0, cudaStream_t st, int64_t* l) {
-  switch (n0) {
-    case 1: return launch_fast<C, 1, F32, BITS>(a, st, l);
-    case 4: return launch_fast<C, 4, F32, BITS>(a, st, l);
-    case 16: return launch_fast<C, 16, F32, BITS>(a, st, l);
-    case 64: return launch_fast<C, 64, F32, BITS>(a, st, l);
-    case 256: return launch_fast<C, 256, F32, BITS>(a, st, l);
+template <int C, int N0, bool F32, int BITS>
+cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  return cudaErrorInvalidValue;
+  K1Args a = a0;
+  const int W = a.team_warps;
+  const size_t rb = (size_t)a.K * (F32 ? 4 : 2);
+  int teams = kK1FThreads / (W * 32);
+  teams = teams < 1 ? 1 : (teams > kK1MaxTeams ? kK1MaxTeams : teams);
+  const int64_t rows_per_sm = (a.M + num_sms - 1) / num_sms;
+  if (teams > rows_per_sm) teams = (int)(rows_per_sm < 1 ? 1 : rows_per_sm);
+  const size_t budget = (size_t)216 * 1024 / kK1FMinBlocks;
+  int S = (int)(budget / ((size_t)teams * rb));
+  if (S > kK1MaxStages) S = kK1MaxStages;
+  const bool bulk = S >= 1 && ((uintptr_t)a.x % 16 == 0) && ((a.ldx * (F32 ? 4 : 2)) % 16 == 0);
+  a.stages = bulk ? S : 1;
+  const int threads = teams * W * 32;
+  const size_t smem = bulk ? (size_t)teams * S * rb : 0;
+  const bool full = a.K / 16 == (int64_t)C * W * 32;  // every lane owns C whole chunks
+  auto kern = bulk ? (full ? k1_fast<C, N0, F32, BITS, true, true>
+                           : k1_fast<C, N0, F32, BITS, true, false>)
+                   : (full ? k1_fast<C, N0, F32, BITS, false, true>
+                           : k1_fast<C, N0, F32, BITS, false, false>);
+  if (bulk) {
+    static size_t smem_set[2] = {0, 0};  // per instantiation, [full]
+    if (smem > smem_set[full]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      smem_set[full] = smem;
+    }
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.M + teams - 1) / teams;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, threads, smem, st>>>(a);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int N0, bool F32, int BITS>
+cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
+  switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
+    case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
+    case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);
+    case 6: return launch_fast<6, N0, F32, BITS>(a, st, l);
+    case 8: return launch_fast<8, N0, F32, BITS>(a, st, l);
+  }
+  return launch_rolled<N0, F32, BITS>(a, st, l);
 }
 
 template <bool F32, int BITS>
-cudaError_t k1_dispatch(const K1Args& a, int c, int n0, cudaStream_t st, int64_t* l) {
-  switch (c) {
-    case 2: return dispatch_n0<2, F32, BITS>(a, n0, st, l);
-    case 4: return dispatch_n0<4, F32, BITS>(a, n0, st, l);
-    case 6: return dispatch_n0<6, F32, BITS>(a, n0, st, l);
-    case 8: return dispatch_n0<8, F32, BITS>(a, n0, st, l);
+cudaError_t k1_dispatch(const K1Args& a, int n0, cudaStream_t st, int64_t* l) {
+  switch (n0) {
+    case 1: return launch_any<1, F32, BITS>(a, st, l);
+    case 4: return launch_any<4, F32, BITS>(a, st, l);
+    case 16: return launch_any<16, F32, BITS>(a, st, l);
+    case 64: return launch_any<64, F32, BITS>(a, st, l);
+    case 256: return launch_any<256, F32, BITS>(a, st, l);
   }
   return cudaErrorInvalidValue;
 }
-
 
 template <bool F32, int BITS>
 cudaError_t k1_exact_launch(const K1Args& a, cudaStream_t st) {

@@ -8,7 +8,7 @@
 namespace crt {
 
 template <bool F32, int BITS>
-cudaError_t k1_dispatch(const K1Args& a, int c, int n0, cudaStream_t st, int64_t* l);
+cudaError_t k1_dispatch(const K1Args& a, int n0, cudaStream_t st, int64_t* l);
 template <bool F32, int BITS>
 cudaError_t k1_exact_launch(const K1Args& a, cudaStream_t st);
 
@@ -30,27 +30,27 @@ K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, in
   (void)identity_tail;
   if (!ok) return p;
   const int64_t nchunks = K / 16;
-  // pick C (chunks per lane) and W (warps per team): exact fit preferred,
-  // W must divide 8 or be >= 8.
-  int bestC = 0, bestW = 0;
-  int64_t best_waste = INT64_MAX;
-  for (int c : {4, 2, 6, 8}) {
-    int64_t w = (nchunks + 32 * c - 1) / (32 * c);
-    if (w > 8) continue;
-    if (w < 8 && 8 % w != 0) {
-      // round W up to a divisor of 8
-      int64_t ww = w;
-      while (8 % ww != 0) ++ww;
-      w = ww;
-    }
-    int64_t waste = w * 32 * c - nchunks;
-    if (waste < best_waste) {
-      best_waste = waste;
-      bestC = c;
-      bestW = (int)w;
+  // Team of W warps per row with C (even) chunks per lane: about 6 chunks
+  // (96 elements) per lane amortises the per-row work (reductions, scale,
+  // certification).  Single-pass kernels hold C <= 8 chunks in registers
+  // with W <= 6 (one 192-thread CTA); wider rows use the rolled two-pass
+  // kernel (W <= 8).
+  int64_t W = (nchunks + 191) / 192;
+  if (W < 1) W = 1;
+  int64_t C = (nchunks + 32 * W - 1) / (32 * W);
+  C += C & 1;
+  if (C < 2) C = 2;
+  if (W > 6) {
+    W = (nchunks + 255) / 256;
+    C = 8;
+    if (W > 6) {  // rolled kernel
+      W = 8;
+      C = (nchunks + 255) / 256;
+      C += C & 1;
+      if (C <= 8) C = 10;
     }
   }
-  if (bestC == 0) return p;
+  const int bestC = (int)C, bestW = (int)W;
   p.fast = true;
   p.C = bestC;
   p.W = bestW;
@@ -62,13 +62,14 @@ cudaError_t launch_k1(const K1Args& a, const K1Plan& p, bool f32, int bits, cuda
   if (p.fast) {
     K1Args b = a;
     b.team_warps = p.W;
+    b.chunks = p.C;
     const int n0 = a.kind == kRotNone ? 1 : (int)a.group;
     if (f32) {
-      return bits == 4 ? k1_dispatch<true, 4>(b, p.C, n0, st, launches)
-                       : k1_dispatch<true, 8>(b, p.C, n0, st, launches);
+      return bits == 4 ? k1_dispatch<true, 4>(b, n0, st, launches)
+                       : k1_dispatch<true, 8>(b, n0, st, launches);
     }
-    return bits == 4 ? k1_dispatch<false, 4>(b, p.C, n0, st, launches)
-                     : k1_dispatch<false, 8>(b, p.C, n0, st, launches);
+    return bits == 4 ? k1_dispatch<false, 4>(b, n0, st, launches)
+                     : k1_dispatch<false, 8>(b, n0, st, launches);
   }
   cudaError_t e = f32 ? (bits == 4 ? k1_exact_launch<true, 4>(a, st) : k1_exact_launch<true, 8>(a, st))
                       : (bits == 4 ? k1_exact_launch<false, 4>(a, st) : k1_exact_launch<false, 8>(a, st));

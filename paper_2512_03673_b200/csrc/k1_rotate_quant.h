@@ -15,6 +15,8 @@ struct K1Args {
   int64_t rot_cols;   // columns covered by whole groups (identity tail beyond)
   int32_t kind;       // kRotNone / kRotSylvester / kRotRegular
   int32_t team_warps; // filled by the plan
+  int32_t stages;     // shared-memory row ring depth (launcher)
+  int32_t chunks;     // 16-element chunks per lane (even; filled by the plan)
   uint8_t* codes;     // M rows x ldc bytes
   int64_t ldc;
   float* s32;         // nullable
@@ -24,7 +26,7 @@ struct K1Args {
 
 struct K1Plan {
   bool fast;
-  int C;  // 16-element chunks per lane
+  int C;  // 16-element chunks per lane (even)
   int W;  // warps per row team
 };
 
