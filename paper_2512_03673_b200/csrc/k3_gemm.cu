@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k3_gemm.h"
@@ -354,6 +355,11 @@ cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int
 void k3_free_weights(K3Weights* w) { w->codes = nullptr; }
 
 cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
+  static const bool force_v1 = [] {
+    const char* e = getenv("CRT_K3_V1");
+    return e && e[0] == '1';
+  }();
+  if (!force_v1 && k3_v2_supported(a)) return k3_v2_launch(a, st, launches);
   const bool b4 = a.bits == 4;
   const bool aligned = ((uintptr_t)a.a_codes % 16 == 0) && (a.lda % 16 == 0) &&
                        ((uintptr_t)a.w.codes % 16 == 0) && (a.w.ld % 16 == 0);

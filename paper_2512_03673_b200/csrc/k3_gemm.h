@@ -37,4 +37,9 @@ cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int
 void k3_free_weights(K3Weights* w);
 cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 
+// v2: persistent 2-SM (cta_group::2) kernel, TMA-staged packed tiles, A
+// expanded into TMEM (k3_gemm_v2.cu).  W4A4 only.
+bool k3_v2_supported(const K3Args& a);
+cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
+
 }  // namespace crt
