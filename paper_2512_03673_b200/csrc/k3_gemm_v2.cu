@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k3_gemm.h"
@@ -47,8 +48,8 @@ constexpr int V2_BN = 192;         // output channels per pair tile
 constexpr int V2_BNH = V2_BN / 2;  // B rows per CTA
 constexpr int V2_BKB = 64;         // packed bytes per row per K block (128 codes)
 constexpr int V2_KS = 4;           // K stages (TMEM A + smem int8 B)
-constexpr int V2_PS = 4;           // packed (TMA) stages
-constexpr int V2_THREADS = 512;
+constexpr int V2_PS = 8;           // packed (TMA) stages
+constexpr int V2_THREADS = 640;  // 20 warps
 constexpr int V2_PK_A = V2_BM * V2_BKB;     // 8 KB
 constexpr int V2_PK_B = V2_BNH * V2_BKB;    // 6 KB
 constexpr int V2_PK_STAGE = 16384;          // A + B, 1 KB aligned
@@ -226,6 +227,7 @@ struct V2Args {
   int64_t ldy;
 };
 
+template <int SKIP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
     k3_v2_kernel(const __grid_constant__ CUtensorMap map_a,
                  const __grid_constant__ CUtensorMap map_b, V2Args a) {
@@ -283,7 +285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         const int m0 = mt * 2 * V2_BM + (int)rank * V2_BM;
         const int n0 = nt * V2_BN + (int)rank * V2_BNH;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait_sleep(&ss->pk_empty[ps], pph ^ 1);
+          mbar_wait(&ss->pk_empty[ps], pph ^ 1);
           uint8_t* st = pk + ps * V2_PK_STAGE;
           mbar_arrive_expect_tx(&ss->pk_full[ps], V2_PK_A + V2_PK_B);
           tma_load_2d(st, &map_a, kb * V2_BKB, m0, &ss->pk_full[ps]);
@@ -361,8 +363,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         }
         mbar_wait(&ss->st_empty[ks], kph ^ 1);
         tc_fence_after();
-        tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col(ks), r);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (SKIP != 1) {
+          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col(ks), r);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(full_st + ks * 8);
@@ -376,14 +380,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 8 && warp < 12) {
+  } else if (warp >= 8 && warp < 16) {
     // ===== B expansion: packed SW64 smem -> int8 x16 -> SW128 K-major tile =====
-    const int e = threadIdx.x - 256;  // 0..127
+    // Two groups of 4 warps take alternate K blocks, so each warp has two
+    // MMA K-block periods to cover its load -> expand -> store -> fence chain.
+    const int grp = (warp - 8) >> 2;
+    const int e = threadIdx.x - 256 - grp * 128;  // 0..127
     const uint32_t full_st = mapa(smem_u32(&ss->st_full[0]), 0);
-    int ps = 0, ks = 0;
-    uint32_t pph = 0, kph = 0;
+    int c = 0;  // global K-block counter of this CTA
     for (int t = pair; t < ntiles; t += npairs) {
-      for (int kb = 0; kb < KB; ++kb) {
+      for (int kb = 0; kb < KB; ++kb, ++c) {
+        if ((c & 1) != grp) continue;
+        const int ps = c % V2_PS, ks = c % V2_KS;
+        const uint32_t pph = (uint32_t)(c / V2_PS) & 1u, kph = (uint32_t)(c / V2_KS) & 1u;
         mbar_wait(&ss->pk_full[ps], pph);
         const uint32_t src = smem_u32(pk + ps * V2_PK_STAGE + V2_PK_A);
         uint4 p[3];
@@ -401,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         mbar_wait(&ss->st_empty[ks], kph ^ 1);
         uint8_t* tile = b8 + ks * V2_B8_STAGE;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < (SKIP == 2 ? 0 : 3); ++i) {
           const int u = e + i * 128;
           const int r = u >> 2, j = u & 3;
           const uint4 v = p[i];
@@ -422,21 +431,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         fence_proxy_async();  // generic-proxy smem writes -> visible to the MMA
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(full_st + ks * 8);
-        if (++ps == V2_PS) {
-          ps = 0;
-          pph ^= 1;
-        }
-        if (++ks == V2_KS) {
-          ks = 0;
-          kph ^= 1;
-        }
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 16) {
     // ===== epilogue: TMEM -> registers -> dequant -> global =====================
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - 384;  // 0..127
+    const int et = threadIdx.x - 512;  // 0..127
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
     int ab = 0;
     uint32_t aph = 0;
@@ -588,17 +589,23 @@ cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.y = a.y;
   v.ldy = a.ldy;
   const size_t smem = 1024 + V2_PS * V2_PK_STAGE + V2_KS * V2_B8_STAGE + sizeof(V2Smem);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k3_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const int skip = [] {  // timing experiments only
+    const char* e = getenv("CRT_K3_SKIP");
+    const int v = e ? atoi(e) : 0;
+    return v >= 0 && v <= 2 ? v : 0;
+  }();
+  auto kern = skip == 1 ? k3_v2_kernel<1> : skip == 2 ? k3_v2_kernel<2> : k3_v2_kernel<0>;
+  static bool attr[3] = {false, false, false};
+  if (!attr[skip]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[skip] = true;
   }
   const int tiles = v.mtiles * v.ntiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  k3_v2_kernel<<<(unsigned)(2 * pairs), V2_THREADS, smem, st>>>(ma, mb, v);
+  kern<<<(unsigned)(2 * pairs), V2_THREADS, smem, st>>>(ma, mb, v);
   ++*launches;
   return cudaGetLastError();
 }
