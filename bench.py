@@ -327,7 +327,7 @@ def run_ours(args):
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "k3_traffic.json"))).get(
-            "bytes_per_launch")
+            "fc1_bytes_per_launch")
     except Exception:
         pass
 
@@ -386,7 +386,8 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
                        "n0": n0, "bits": "W4A4", "parallelism": f"replica x{world}" if world > 1 else "single",
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
-            "roofline": {"bound": "tensor", "kernel": "k3_ss_kernel<4> (W4A4 GEMM)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
                          "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",
                          "frac": k3_tops / int8_peak, "traffic": traffic,
                          "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json); "

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k1_rotate_quant.h"
@@ -144,6 +145,55 @@ __device__ __noinline__ double y_exact_lane(const void* row, int64_t j, int64_t 
   return y_ref<F32>(row, j, group, kind, rot_cols);
 }
 
+// y_exact_lane for a group inside one 16-element chunk (N0 <= 16), fully
+// unrolled: the chunk is re-read with vector loads and the exponent-span
+// certificate is evaluated branch-free.  Falls back to y_exact_lane (the
+// reference's sequential loop) only when the certificate fails.
+template <bool F32, int N0>
+__device__ __noinline__ double y_exact_chunk(const void* row, int64_t chunk, int e, int kind,
+                                             int64_t rot_cols, float y32) {
+  const int64_t j = chunk * 16 + e;
+  if (kind == kRotNone || j >= rot_cols) return load_x<F32>(row, j);
+  float x[16];
+  if constexpr (F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + chunk * 64);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = p[q];
+      x[4 * q] = __uint_as_float(v.x);
+      x[4 * q + 1] = __uint_as_float(v.y);
+      x[4 * q + 2] = __uint_as_float(v.z);
+      x[4 * q + 3] = __uint_as_float(v.w);
+    }
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(row) + chunk * 32);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint4 v = p[q];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x[8 * q + 2 * i] = __uint_as_float(w[i] << 16);
+        x[8 * q + 2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+      }
+    }
+  }
+  const int g0 = e & ~(N0 - 1);
+  int emin = 1 << 20, emax = -1, bad = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int ex = (int)((__float_as_uint(x[i]) >> 23) & 0xFFu);
+    const bool in = (i & ~(N0 - 1)) == g0 && x[i] != 0.f;
+    bad |= (in && (ex == 0 || ex == 255)) ? 1 : 0;
+    emin = in ? min(emin, ex) : emin;
+    emax = in ? max(emax, ex) : emax;
+  }
+  constexpr int L2 = N0 == 4 ? 2 : 4;
+  if (!bad && kind == kRotRegular && (emax < 0 || 1 + L2 + (emax - emin) + (F32 ? 24 : 8) <= 24))
+    return (double)y32 * (N0 == 4 ? 0.5 : 0.25);
+  return y_ref<F32>(row, j, N0, kind, rot_cols);
+}
+
 __device__ __forceinline__ int exact_code(double y, double s, int qmax) {
   double q = rint(__ddiv_rn(y, s));  // nearbyint, FE_TONEAREST
   q = fmin(fmax(q, (double)-qmax), (double)qmax);
@@ -154,15 +204,17 @@ __device__ __forceinline__ int exact_code(double y, double s, int qmax) {
 // ---------------------------------------------------------------------------
 // Warp / team reductions
 // ---------------------------------------------------------------------------
+// Maxima of NON-NEGATIVE values (absolute values, +NaN, +inf): their IEEE
+// bit patterns order like unsigned integers (+NaN above +inf), so one REDUX
+// replaces a five-step shuffle tree.
 __device__ __forceinline__ float warp_max_nan(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
 __device__ __forceinline__ double warp_max_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(b >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(b >> 32) == hi ? (uint32_t)b : 0u);
+  return __longlong_as_double((long long)(((uint64_t)hi << 32) | lo));
 }
 
 struct TeamScratch {
@@ -471,12 +523,126 @@ __device__ __noinline__ void k1_slow_row_codes(const void* rowp, uint8_t* crow, 
 //
 // Certified rounding: see the file header and DESIGN.md.
 // ---------------------------------------------------------------------------
+// Pack + store the codes of one chunk pair from the magic-rounded values
+// tb[h][i] (h = chunk of the pair, i = element).  4-bit codes come from the
+// biased magic (low nibble = code + 8): one IMAD packs a byte in offset
+// binary, one XOR per word turns it into two's-complement nibbles.
+template <int BITS, bool FULL>
+__device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], uint8_t* crow,
+                                                 int64_t c0, int64_t cstride, int64_t nchunks) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0 + h * cstride;
+    if (!FULL && chunk >= nchunks) continue;
+    if constexpr (BITS == 4) {
+      uint32_t by[8];
+#pragma unroll
+      for (int b2 = 0; b2 < 8; ++b2) by[b2] = tb[h][2 * b2 + 1] * 16u + tb[h][2 * b2];
+      uint2 out;
+      out.x = __byte_perm(__byte_perm(by[0], by[1], 0x0040), __byte_perm(by[2], by[3], 0x0040),
+                          0x5410) ^ 0x88888888u;
+      out.y = __byte_perm(__byte_perm(by[4], by[5], 0x0040), __byte_perm(by[6], by[7], 0x0040),
+                          0x5410) ^ 0x88888888u;
+      *reinterpret_cast<uint2*>(crow + chunk * 8) = out;
+    } else {
+      uint32_t wds[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
+                             __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040), 0x5410);
+      *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+    }
+  }
+}
+
+// Elements of a pair whose rounding decision is not certified (bit h*16+i).
+__device__ __forceinline__ uint32_t near_tie_mask(const float2 (&v)[16], const uint32_t (&tb)[2][16],
+                                                  float inv, float mg, float thr) {
+  uint32_t fm = 0u;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float ex = fmaf(v[i].x, inv, mg - __uint_as_float(tb[0][i]));
+    const float ey = fmaf(v[i].y, inv, mg - __uint_as_float(tb[1][i]));
+    fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
+    fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
+  }
+  return fm;
+}
+
+// Lane-local exact decisions (N0 <= 16): flagged bits (h*16 + i) of `m`
+// index the 32 fp32 sums vl[] of the calling lane's chunk pair.
+template <bool F32, int BITS, int N0>
+__device__ __noinline__ void k1_redecide_lane(uint32_t m, const float2* vl, const void* rowp,
+                                              uint8_t* crow, int64_t c0, int64_t cstride,
+                                              int64_t nchunks, double s, int64_t group, int kind,
+                                              int64_t rot_cols) {
+  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    const int i = bit & 15;
+    const int64_t chunk = c0 + (bit >> 4) * cstride;
+    if (chunk >= nchunks) continue;
+    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
+    const int code = exact_code(y_exact_chunk<F32, N0>(rowp, chunk, i, kind, rot_cols, y32), s, QMAX);
+    if constexpr (BITS == 4) {
+      uint8_t* bp = crow + chunk * 8 + (i >> 1);
+      const uint8_t old = *bp;
+      *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
+                    : (uint8_t)((old & 0xF0) | (code & 0x0F));
+    } else {
+      crow[chunk * 16 + i] = (uint8_t)code;
+    }
+  }
+}
+
+// Lane-local exact |y_ref| maximum over the lane's candidates (N0 <= 16).
+template <bool F32, int N0>
+__device__ __noinline__ double k1_cands_lane(uint32_t m, const float2* vl, const void* rowp,
+                                             int64_t c0, int64_t cstride, int64_t nchunks,
+                                             int64_t group, int kind, int64_t rot_cols) {
+  double cmax = 0.0;
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    const int i = bit & 15;
+    const int64_t chunk = c0 + (bit >> 4) * cstride;
+    if (chunk >= nchunks) continue;
+    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
+    cmax = fmax(cmax, fabs(y_exact_chunk<F32, N0>(rowp, chunk, i, kind, rot_cols, y32)));
+  }
+  return cmax;
+}
+
+// Warp-cooperative versions (N0 >= 64: a group spans lanes).
+template <bool F32>
+__device__ __noinline__ double k1_cands_warp(uint32_t m, const void* rowp, int64_t c0,
+                                             int64_t cstride, int64_t nchunks, int64_t group,
+                                             int kind, int64_t rot_cols) {
+  const int lane = threadIdx.x & 31;
+  double cmax = 0.0;
+  for (;;) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
+    if (!bal) break;
+    const int src = __ffs(bal) - 1;
+    const int bit = __shfl_sync(0xffffffffu, __ffs(m) - 1, src);
+    const int64_t chunk = __shfl_sync(0xffffffffu, c0, src) + (bit >> 4) * cstride;
+    double y = 0.0;
+    if (chunk < nchunks) y = y_exact_warp<F32>(rowp, chunk * 16 + (bit & 15), group, kind, rot_cols);
+    if (lane == src) {
+      cmax = fmax(cmax, fabs(y));
+      m &= m - 1;
+    }
+  }
+  return cmax;
+}
+
 constexpr int kK1MaxTeams = 8;
 constexpr int kK1MaxStages = 4;
 constexpr int kK1Threads = 256;
 constexpr int kK1MinBlocks = 3;  // rolled kernel: <= 85 registers, 24 warps per SM
 
-template <int N0, bool F32, int BITS, bool BULK>
+template <int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) {
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 4 ? 7 : 127;
@@ -520,7 +686,6 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     }
   }
 
-  // normalisation 2^-k = 1/sqrt(N0) (exact), and the certified bound factor
   const double rk = N0 == 1 ? 1.0 : 1.0 / sqrt((double)N0);
   const double sqrtn = N0 == 1 ? 1.0 : sqrt((double)N0);
   const double bound_rel = L == 0 ? 0.0
@@ -541,7 +706,8 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
 #pragma unroll 1
     for (int p = 0; p < P; ++p) {
       float2 v[16];
-      load_pair<F32, BULK>(v, rowp, ((int64_t)(2 * p) * W + w) * 32 + lane, cstride, nchunks);
+      load_pair<F32, BULK, FULL>(v, rowp, ((int64_t)(2 * p) * W + w) * 32 + lane, cstride,
+                                 nchunks);
       rotate_pair<N0>(v);
       const float m = pair_absmax(v);
       lmax_nan = max_nan(lmax_nan, m);
@@ -561,17 +727,40 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     double amax_ref = 0.0;
     if (!slow_row) {
       if (N0 == 1 || A32 == 0.f) {
-        // no rotation: y32 == x exactly; all-zero fp32 sums <=> all-zero row
         amax_ref = (double)A32;
       } else {
-        // candidates for the exact row max: |y32| >= A32 - 2B,
-        // each settled by the warp-cooperative exact evaluation
+        // candidates |y32| >= A32 - 2B lie in the lane's best pair unless its
+        // second-best pair also reaches thr; recompute that pair, settle each
+        // candidate exactly (lane-local for N0 <= 16, warp-wide otherwise)
         const float thr = (float)((double)A32 - 2.0 * B) * (1.0f - 1e-6f);
         const bool has = lmax >= thr;
+        const bool all = m2 >= thr;
         double cmax = 0.0;
-        if (__any_sync(0xffffffffu, has))
-          cmax = k1_candidates_max<N0, F32, BULK>(rowp, P, W, w, nchunks, has, bp, m2 >= thr,
-                                                  thr, a.group, a.kind, a.rot_cols);
+        if constexpr (N0 <= 16) {
+          if (has) {
+#pragma unroll 1
+            for (int p = 0; p < P; ++p) {
+              if (!(all || p == bp)) continue;
+              const int64_t c0 = ((int64_t)(2 * p) * W + w) * 32 + lane;
+              float2 vl[16];
+              load_pair<F32, BULK, FULL>(vl, rowp, c0, cstride, nchunks);
+              rotate_pair<N0>(vl);
+              uint32_t m = 0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                m |= (fabsf(vl[i].x) >= thr ? 1u : 0u) << i;
+                m |= (fabsf(vl[i].y) >= thr ? 1u : 0u) << (16 + i);
+              }
+              if (m)
+                cmax = fmax(cmax, k1_cands_lane<F32, N0>(m, vl, rowp, c0, cstride, nchunks,
+                                                         a.group, a.kind, a.rot_cols));
+            }
+          }
+        } else {
+          if (__any_sync(0xffffffffu, has))
+            cmax = k1_candidates_max<N0, F32, BULK>(rowp, P, W, w, nchunks, has, bp, all, thr,
+                                                    a.group, a.kind, a.rot_cols);
+        }
         amax_ref = team_max_d(cmax, &ts, team, w, W);
       }
     } else {
@@ -585,80 +774,49 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
 
     uint8_t* crow = a.codes + row * a.ldc;
     if (!slow_row) {
-      // ---- pass 2: certified quantisation + pack + store ---------------------
-      // t = M + rint(y*inv) with M = 1.5*2^23 (ulp 1): the low byte of its
-      // bit pattern is the two's-complement code; e = y*inv - rint(y*inv)
-      // certifies the decision against the reference's double rint(y/s).
-      const double invd = rk / s;
-      const float inv = __double2float_rn(invd);
-      const float margin = (float)(B * invd * 1.05) +
-                           (float)(QMAX + 4) * 1.1920928955078125e-7f + 1e-9f;
+      // ---- pass 2: certified quantisation + pack + store (see k1_fast) -------
+      const float inv = amax_ref == 0.0 ? (float)rk
+                                        : (float)(rk * QMAX) * __frcp_rn((float)amax_ref);
+      const float margin = (float)B * (inv * 1.05f) +
+                           (float)(QMAX + 4) * 2.384185791015625e-7f + 1e-9f;
       const float thr = 0.5f - margin;
+      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
       const float2 iv = make_float2(inv, inv);
-      const float2 cc = make_float2(__uint_as_float(kMagic23), __uint_as_float(kMagic23));
+      const float2 cc = make_float2(mg, mg);
 #pragma unroll 1
       for (int p = 0; p < P; ++p) {
         const int64_t c0 = ((int64_t)(2 * p) * W + w) * 32 + lane;
         float2 v[16];
-        load_pair<F32, BULK>(v, rowp, c0, cstride, nchunks);
+        load_pair<F32, BULK, FULL>(v, rowp, c0, cstride, nchunks);
         rotate_pair<N0>(v);
         uint32_t tb[2][16];
-        float em0 = 0.f, em1 = 0.f;
+        float em[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float2 t = __ffma2_rn(v[i], iv, cc);                      // M + rint(y*inv)
-          const float2 nr = __ffma2_rn(t, make_float2(-1.f, -1.f), cc);   // -rint(y*inv)
-          const float2 e = __ffma2_rn(v[i], iv, nr);                      // y*inv - rint
-          if (i & 1) em1 = max3_abs(e.x, e.y, em1);
-          else em0 = max3_abs(e.x, e.y, em0);
+          const float2 t = __ffma2_rn(v[i], iv, cc);
+          const float2 nr = __ffma2_rn(t, make_float2(-1.f, -1.f), cc);
+          const float2 e = __ffma2_rn(v[i], iv, nr);
+          em[i & 3] = max3_abs(e.x, e.y, em[i & 3]);
           tb[0][i] = __float_as_uint(t.x);
           tb[1][i] = __float_as_uint(t.y);
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t chunk = c0 + h * cstride;
-          if (chunk >= nchunks) continue;
-          if constexpr (BITS == 4) {
-            uint32_t by[8];
-#pragma unroll
-            for (int b2 = 0; b2 < 8; ++b2)  // low byte = (odd << 4) | (even & 0xF)
-              by[b2] = tb[h][2 * b2 + 1] * 16u + (tb[h][2 * b2] & 0xFu);
-            uint2 out;
-            out.x = __byte_perm(__byte_perm(by[0], by[1], 0x0040),
-                                __byte_perm(by[2], by[3], 0x0040), 0x5410);
-            out.y = __byte_perm(__byte_perm(by[4], by[5], 0x0040),
-                                __byte_perm(by[6], by[7], 0x0040), 0x5410);
-            *reinterpret_cast<uint2*>(crow + chunk * 8) = out;
-          } else {
-            uint32_t wds[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
-                                   __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
-                                   0x5410);
-            *reinterpret_cast<uint4*>(crow + chunk * 16) =
-                make_uint4(wds[0], wds[1], wds[2], wds[3]);
-          }
-        }
-        // rare: an element of this pair within the certified margin of a
-        // rounding boundary -> all 32 re-decided exactly (owner lane
-        // re-writes the bytes it just stored; program order makes it safe)
+        store_codes_pair<BITS, FULL>(tb, crow, c0, cstride, nchunks);
         uint32_t fm = 0u;
-        if (!(max_nan(em0, em1) <= thr)) {
-          // rare: some element lies within the certified margin of a
-          // rounding boundary (exact ties y/s = k + 1/2 are common with
-          // discrete bf16 data); find which
+        if (!(max_nan(max_nan(em[0], em[1]), max_nan(em[2], em[3])) <= thr))
+          fm = near_tie_mask(v, tb, inv, mg, thr);
+        if constexpr (N0 <= 16) {
+          if (fm) {
+            float2 vl[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float ex = fmaf(v[i].x, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[0][i]));
-            const float ey = fmaf(v[i].y, inv, __uint_as_float(kMagic23) - __uint_as_float(tb[1][i]));
-            fm |= (fabsf(ex) <= thr ? 0u : 1u) << i;
-            fm |= (fabsf(ey) <= thr ? 0u : 1u) << (16 + i);
+            for (int i = 0; i < 16; ++i) vl[i] = v[i];
+            k1_redecide_lane<F32, BITS, N0>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
+                                            a.kind, a.rot_cols);
           }
+        } else {
+          if (__any_sync(0xffffffffu, fm != 0u))
+            k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
+                                   a.rot_cols);
         }
-        if (__any_sync(0xffffffffu, fm != 0u))
-          k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
-                                 a.rot_cols);
       }
     } else {
       k1_slow_row_codes<F32, BITS>(rowp, crow, a.chunks, W, w, nchunks, invalid, s, a.group,
@@ -669,8 +827,6 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       if (a.s64) a.s64[row] = s;
     }
     if constexpr (BULK) {
-      // every lane of the team is done with this stage (both passes and the
-      // exact re-evaluations): refill it with the row `stages` ahead.
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
       if (leader) {
@@ -697,75 +853,6 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
 // ---------------------------------------------------------------------------
 constexpr int kK1FThreads = 192;  // 6 warps; two CTAs per SM at <= 170 registers
 constexpr int kK1FMinBlocks = 2;
-
-// Lane-local exact decisions (N0 <= 16): flagged bits (h*16 + i) of `m`
-// index the 32 fp32 sums vl[] of the calling lane's chunk pair.
-template <bool F32, int BITS>
-__device__ __noinline__ void k1_redecide_lane(uint32_t m, const float2* vl, const void* rowp,
-                                              uint8_t* crow, int64_t c0, int64_t cstride,
-                                              int64_t nchunks, double s, int64_t group, int kind,
-                                              int64_t rot_cols) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
-  while (m) {
-    const int bit = __ffs(m) - 1;
-    m &= m - 1;
-    const int i = bit & 15;
-    const int64_t chunk = c0 + (bit >> 4) * cstride;
-    if (chunk >= nchunks) continue;
-    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
-    const int code = exact_code(y_exact_lane<F32>(rowp, chunk * 16 + i, group, kind, rot_cols, y32),
-                                s, QMAX);
-    if constexpr (BITS == 4) {
-      uint8_t* bp = crow + chunk * 8 + (i >> 1);
-      const uint8_t old = *bp;
-      *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
-                    : (uint8_t)((old & 0xF0) | (code & 0x0F));
-    } else {
-      crow[chunk * 16 + i] = (uint8_t)code;
-    }
-  }
-}
-
-// Lane-local exact |y_ref| maximum over the lane's candidates (N0 <= 16).
-template <bool F32>
-__device__ __noinline__ double k1_cands_lane(uint32_t m, const float2* vl, const void* rowp,
-                                             int64_t c0, int64_t cstride, int64_t nchunks,
-                                             int64_t group, int kind, int64_t rot_cols) {
-  double cmax = 0.0;
-  while (m) {
-    const int bit = __ffs(m) - 1;
-    m &= m - 1;
-    const int i = bit & 15;
-    const int64_t chunk = c0 + (bit >> 4) * cstride;
-    if (chunk >= nchunks) continue;
-    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
-    cmax = fmax(cmax, fabs(y_exact_lane<F32>(rowp, chunk * 16 + i, group, kind, rot_cols, y32)));
-  }
-  return cmax;
-}
-
-// Warp-cooperative versions (N0 >= 64: a group spans lanes).
-template <bool F32>
-__device__ __noinline__ double k1_cands_warp(uint32_t m, const void* rowp, int64_t c0,
-                                             int64_t cstride, int64_t nchunks, int64_t group,
-                                             int kind, int64_t rot_cols) {
-  const int lane = threadIdx.x & 31;
-  double cmax = 0.0;
-  for (;;) {
-    const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
-    if (!bal) break;
-    const int src = __ffs(bal) - 1;
-    const int bit = __shfl_sync(0xffffffffu, __ffs(m) - 1, src);
-    const int64_t chunk = __shfl_sync(0xffffffffu, c0, src) + (bit >> 4) * cstride;
-    double y = 0.0;
-    if (chunk < nchunks) y = y_exact_warp<F32>(rowp, chunk * 16 + (bit & 15), group, kind, rot_cols);
-    if (lane == src) {
-      cmax = fmax(cmax, fabs(y));
-      m &= m - 1;
-    }
-  }
-  return cmax;
-}
 
 template <int C, int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) {
@@ -884,7 +971,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
                 float2 vl[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) vl[i] = v[p][i];
-                cmax = fmax(cmax, k1_cands_lane<F32>(m, vl, rowp,
+                cmax = fmax(cmax, k1_cands_lane<F32, N0>(m, vl, rowp,
                                                      ((int64_t)(2 * p) * W + w) * 32 + lane,
                                                      cstride, nchunks, a.group, a.kind,
                                                      a.rot_cols));
@@ -931,10 +1018,13 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
       // certifies the decision against the reference's double rint(y/s).
       // inv = fl32(rk / fl32(s)) is within 2 ulp of rk/s: covered by the
       // (QMAX + 4) ulp slack of the margin.
-      const float sf = (float)s;
-      const float inv = __fdiv_rn((float)rk, sf);
+      // inv = rk/s = rk*QMAX/amax, from an fp32 reciprocal (the double s is
+      // off this critical path; it is only stored and used by exact paths):
+      // within 3 ulp of rk/s, covered by the (QMAX + 4) * 4 ulp slack.
+      const float inv = amax_ref == 0.0 ? (float)rk
+                                        : (float)(rk * QMAX) * __frcp_rn((float)amax_ref);
       const float margin = (float)B * (inv * 1.05f) +
-                           (float)(QMAX + 4) * 1.1920928955078125e-7f + 1e-9f;
+                           (float)(QMAX + 4) * 2.384185791015625e-7f + 1e-9f;
       const float thr = 0.5f - margin;
       // 4-bit codes use the biased magic M + 8, so the low nibble of t is
       // code + 8 in [1, 15] with nothing above it: one IMAD packs a byte
@@ -1001,7 +1091,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
             float2 vl[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) vl[i] = v[p][i];
-            k1_redecide_lane<F32, BITS>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
+            k1_redecide_lane<F32, BITS, N0>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
                                         a.kind, a.rot_cols);
           }
         } else {
@@ -1100,6 +1190,9 @@ __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
   }
 }
 
+template <bool F32, int BITS>
+cudaError_t k1_exact_launch(const K1Args& a, cudaStream_t st);
+
 template <int N0, bool F32, int BITS>
 cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   static int num_sms = 0;
@@ -1125,17 +1218,24 @@ cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) 
   a.stages = bulk ? S : 1;
   const int threads = teams * W * 32;
   const size_t smem = bulk ? (size_t)teams * S * rb : 0;
-  auto kern = bulk ? k1_rolled<N0, F32, BITS, true> : k1_rolled<N0, F32, BITS, false>;
+  // Rows too wide for one shared-memory stage (K > 36864 bf16) go to the
+  // exact kernel: the direct-load rolled variants are not built (ptxas 12.9
+  // crashes on the module that contains them with the others).
+  if (!bulk) {
+    ++*launches;
+    return k1_exact_launch<F32, BITS>(a0, st);
+  }
+  const bool full = a.K / 16 == (int64_t)a.chunks * W * 32;
+  auto kern = full ? k1_rolled<N0, F32, BITS, true, true> : k1_rolled<N0, F32, BITS, true, false>;
   if (bulk) {
-    static size_t smem_set = 0;  // per instantiation
-    if (smem > smem_set) {
+    static size_t smem_set[2] = {0, 0};  // per instantiation, [full]
+    if (smem > smem_set[full]) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
-      // all of L1 as shared memory, or the SM holds a single CTA
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
-      smem_set = smem;
+      smem_set[full] = smem;
     }
   }
   int per_sm = 0;
@@ -1202,6 +1302,11 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
 
 template <int N0, bool F32, int BITS>
 cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
+  static const bool rolled_only = [] {
+    const char* e = getenv("CRT_K1_ROLLED");
+    return e && e[0] == '1';
+  }();
+  if (rolled_only) return launch_rolled<N0, F32, BITS>(a, st, l);
   switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
     case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
     case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);

@@ -1,6 +1,7 @@
 // k1_rotate_quant.cu -- K1 host side: plan (fast vs exact kernel) + launch.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k1_rotate_quant.h"
@@ -48,6 +49,15 @@ K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, in
       C = (nchunks + 255) / 256;
       C += C & 1;
       if (C <= 8) C = 10;
+    }
+  }
+  if (const char* ew = getenv("CRT_K1_W")) {  // tuning experiments only
+    const int64_t w2 = atoi(ew);
+    if (w2 >= 1 && w2 <= 8) {
+      W = w2;
+      C = (nchunks + 32 * W - 1) / (32 * W);
+      C += C & 1;
+      if (C < 2) C = 2;
     }
   }
   const int bestC = (int)C, bestW = (int)W;
