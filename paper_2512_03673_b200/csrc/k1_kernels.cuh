@@ -1306,7 +1306,10 @@ cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
     const char* e = getenv("CRT_K1_ROLLED");
     return e && e[0] == '1';
   }();
-  if (rolled_only) return launch_rolled<N0, F32, BITS>(a, st, l);
+  // Multi-warp rows: the rolled kernel's occupancy (24 warps/SM) beats the
+  // register-resident one (measured: K=12288 N0=16 67.6 vs 77.8 us); one
+  // warp per row (K <= 3072): the single-pass kernel (24.6 vs 28.8 us).
+  if (rolled_only || a.team_warps > 1) return launch_rolled<N0, F32, BITS>(a, st, l);
   switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
     case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
     case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);
