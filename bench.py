@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--parallel", choices=["replica", "column"], default="replica",
+                    help="N>1: independent prompt replicas (weak scaling, default) or "
+                         "column-parallel fc1/fc2 with an NCCL all-gather (strong scaling)")
     return ap.parse_args()
 
 
@@ -226,9 +229,15 @@ def run_ours(args):
     w2 = torch.randn(D_MODEL, D_FF, device=dev, generator=gw).to(torch.bfloat16)
     b1 = torch.randn(D_FF, device=dev, generator=gw)
     b2 = torch.randn(D_MODEL, device=dev, generator=gw)
-    fc1 = crt.prepare_layer(w1, b1, spec, QuantSpec(4), "fc1")
-    fc2 = crt.prepare_layer(w2, b2, spec, QuantSpec(4), "fc2")
+    column = args.parallel == "column" and world > 1
+    if column:  # SURVEY.md 8e / configs[4]: output channels sharded, X replicated
+        fc1 = crt.prepare_layer_shard(w1, b1, spec, QuantSpec(4), rank, world, "fc1")
+        fc2 = crt.prepare_layer_shard(w2, b2, spec, QuantSpec(4), rank, world, "fc2")
+    else:
+        fc1 = crt.prepare_layer(w1, b1, spec, QuantSpec(4), "fc1")
+        fc2 = crt.prepare_layer(w2, b2, spec, QuantSpec(4), "fc2")
     del w1, w2
+    n1, n2 = fc1.out_features, fc2.out_features  # per-rank columns
 
     # preallocated device buffers (no allocation in the timed region)
     ld1 = (D_MODEL // 2 + 15) // 16 * 16
@@ -239,6 +248,12 @@ def run_ours(args):
     s2 = torch.empty(M_TOK, dtype=torch.float32, device=dev)
     y1 = torch.empty(M_TOK, D_FF, dtype=torch.bfloat16, device=dev)
     y2 = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16, device=dev)
+    if column:
+        from paper_2512_03673_b200.parallel import interleave_rank_major
+        y1s = torch.empty(M_TOK, n1, dtype=torch.bfloat16, device=dev)
+        y2s = torch.empty(M_TOK, n2, dtype=torch.bfloat16, device=dev)
+        g1 = torch.empty(world * M_TOK, n1, dtype=torch.bfloat16, device=dev)
+        g2 = torch.empty(world * M_TOK, n2, dtype=torch.bfloat16, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -261,13 +276,23 @@ def run_ours(args):
         k1(x, c1, s1, D_MODEL, ld1)
         if record:
             ev[1].record(stream)
-        k3(c1, ld1, s1, fc1, y1, D_FF)
+        if column:
+            k3(c1, ld1, s1, fc1, y1s, n1)
+            dist.all_gather_into_tensor(g1, y1s)
+            y1.copy_(interleave_rank_major(g1, world))
+        else:
+            k3(c1, ld1, s1, fc1, y1, D_FF)
         if record:
             ev[2].record(stream)
         k1(y1, c2, s2, D_FF, ld2)
         if record:
             ev[3].record(stream)
-        k3(c2, ld2, s2, fc2, y2, D_MODEL)
+        if column:
+            k3(c2, ld2, s2, fc2, y2s, n2)
+            dist.all_gather_into_tensor(g2, y2s)
+            y2.copy_(interleave_rank_major(g2, world))
+        else:
+            k3(c2, ld2, s2, fc2, y2, D_MODEL)
         if record:
             ev[4].record(stream)
 
@@ -308,11 +333,13 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     ops = layer_ops()
-    value = world * ops / (ms_step * 1e-3) / 1e12
+    # replicas: every rank runs the whole pair on its own prompt (weak);
+    # column: the ranks share one pair (strong)
+    value = (1 if column else world) * ops / (ms_step * 1e-3) / 1e12
 
     # roofline of the dominant kernel (K3), measured live on the launching stream
     k3_us = (statistics.mean(seg["k3_fc1"]) + statistics.mean(seg["k3_fc2"])) / 2 * 1e3
-    k3_ops_per_launch = 2 * M_TOK * D_FF * D_MODEL  # both launches do 2*4608*3072*12288
+    k3_ops_per_launch = 2 * M_TOK * D_FF * D_MODEL // (world if column else 1)
     k3_tops = k3_ops_per_launch / (k3_us * 1e-6) / 1e12
     peaks = {}
     try:
@@ -331,37 +358,69 @@ def run_ours(args):
     except Exception:
         pass
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with HOST buffers.  Every step copies its
+    # input from pinned host memory, runs fc1 + fc2 and copies its result
+    # back; steps are software-pipelined over NB streams / buffer sets (as a
+    # serving loop would), so step k+1's upload and step k-1's download run
+    # under step k's kernels.  Also reported: the unpipelined per-step latency.
     e2e = None
-    if not args.no_e2e and not args.profile:
+    if not args.no_e2e and not args.profile and not column:
+        NB = 3
         xh = x.cpu().pin_memory()
-        yh = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16).pin_memory()
-        ws = crt.Workspace(M_TOK, D_FF, dev)
-        def e2e_step():
-            xd = xh.to(dev, non_blocking=True)
-            h = crt.forward(xd, fc1, QuantSpec(4), out="bf16", y=y1, workspace=ws)
-            o = crt.forward(h, fc2, QuantSpec(4), out="bf16", y=y2, workspace=ws)
-            yh.copy_(o, non_blocking=True)
-        for _ in range(3):
-            e2e_step()
+        streams = [torch.cuda.Stream(dev) for _ in range(NB)]
+        bufs = [{"xd": torch.empty_like(x),
+                 "y1": torch.empty(M_TOK, D_FF, dtype=torch.bfloat16, device=dev),
+                 "y2": torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16, device=dev),
+                 "yh": torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16).pin_memory(),
+                 "ws": crt.Workspace(M_TOK, D_FF, dev)} for _ in range(NB)]
+
+        def e2e_step(k):
+            b, st = bufs[k % NB], streams[k % NB]
+            with torch.cuda.stream(st):
+                b["xd"].copy_(xh, non_blocking=True)
+                h = crt.forward(b["xd"], fc1, QuantSpec(4), out="bf16", y=b["y1"],
+                                workspace=b["ws"])
+                o = crt.forward(h, fc2, QuantSpec(4), out="bf16", y=b["y2"], workspace=b["ws"])
+                b["yh"].copy_(o, non_blocking=True)
+
+        for k in range(2 * NB):
+            e2e_step(k)
         torch.cuda.synchronize()
-        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n_e2e = max(3, args.steps // 2)
-        times = []
-        for _ in range(n_e2e):
-            es.record(stream)
-            e2e_step()
-            ee.record(stream)
-            ee.synchronize()
-            times.append(es.elapsed_time(ee))
-        e_ms = statistics.mean(times)
+        n_e2e = max(3 * NB, args.steps)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(streams[0])
+        for st in streams[1:]:
+            st.wait_event(e0)
+        for k in range(n_e2e):
+            e2e_step(k)
+        ends = []
+        for st in streams:
+            ev_end = torch.cuda.Event(enable_timing=True)
+            ev_end.record(st)
+            ends.append(ev_end)
+        torch.cuda.synchronize()
+        e_ms = max(e0.elapsed_time(ev_end) for ev_end in ends) / n_e2e
+        # unpipelined latency of one step (same copies, one stream)
+        lat = []
+        for k in range(NB):
+            la, lb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            la.record(streams[0])
+            e2e_step(0)
+            lb.record(streams[0])
+            lb.synchronize()
+            lat.append(la.elapsed_time(lb))
         if world > 1:
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": world * ops / (e_ms * 1e-3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": xh.numel() * 2, "d2h_bytes_per_step": yh.numel() * 2,
-               "ms_per_step": e_ms}
+               "h2d_bytes_per_step": xh.numel() * 2,
+               "d2h_bytes_per_step": bufs[0]["yh"].numel() * 2,
+               "ms_per_step": e_ms, "pipelined_streams": NB,
+               "step_latency_ms": statistics.median(lat)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -381,10 +440,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int4",
+            "higher_is_better": True, "scaling": "strong" if column else "weak",
+            "vs_baseline": None, "dtype": "int4",
             "data": "synthetic (seeded gaussian bf16 activations, random-init weights)",
             "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
-                       "n0": n0, "bits": "W4A4", "parallelism": f"replica x{world}" if world > 1 else "single",
+                       "n0": n0, "bits": "W4A4",
+                       "parallelism": (f"column-parallel x{world} + NCCL all-gather" if column else
+                                       f"prompt replicas x{world}" if world > 1 else "single"),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "roofline": {"bound": "tensor",
                          "kernel": "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",

@@ -1272,12 +1272,13 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   a.stages = bulk ? S : 1;
   const int threads = teams * W * 32;
   const size_t smem = bulk ? (size_t)teams * S * rb : 0;
+  if (!bulk) {  // unaligned rows: exact kernel (direct-load variants not built)
+    ++*launches;
+    return k1_exact_launch<F32, BITS>(a0, st);
+  }
   const bool full = a.K / 16 == (int64_t)C * W * 32;  // every lane owns C whole chunks
-  auto kern = bulk ? (full ? k1_fast<C, N0, F32, BITS, true, true>
-                           : k1_fast<C, N0, F32, BITS, true, false>)
-                   : (full ? k1_fast<C, N0, F32, BITS, false, true>
-                           : k1_fast<C, N0, F32, BITS, false, false>);
-  if (bulk) {
+  auto kern = full ? k1_fast<C, N0, F32, BITS, true, true> : k1_fast<C, N0, F32, BITS, true, false>;
+  {
     static size_t smem_set[2] = {0, 0};  // per instantiation, [full]
     if (smem > smem_set[full]) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1300,16 +1301,22 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   return cudaGetLastError();
 }
 
+}  // namespace crt
+#include "k1_mma.cuh"
+namespace crt {
+
 template <int N0, bool F32, int BITS>
 cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
-  static const bool rolled_only = [] {
-    const char* e = getenv("CRT_K1_ROLLED");
-    return e && e[0] == '1';
-  }();
   // Multi-warp rows: the rolled kernel's occupancy (24 warps/SM) beats the
   // register-resident one (measured: K=12288 N0=16 67.6 vs 77.8 us); one
   // warp per row (K <= 3072): the single-pass kernel (24.6 vs 28.8 us).
-  if (rolled_only || a.team_warps > 1) return launch_rolled<N0, F32, BITS>(a, st, l);
+  if constexpr (!F32 && (N0 == 4 || N0 == 16)) {
+    if (mma_path_ok(a, N0, F32)) {
+      const cudaError_t e = launch_mma<N0, BITS>(a, st, l);
+      if (e != cudaErrorInvalidValue) return e;
+    }
+  }
+  if (a.team_warps > 1) return launch_rolled<N0, F32, BITS>(a, st, l);
   switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
     case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
     case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);

@@ -51,15 +51,6 @@ K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, in
       if (C <= 8) C = 10;
     }
   }
-  if (const char* ew = getenv("CRT_K1_W")) {  // tuning experiments only
-    const int64_t w2 = atoi(ew);
-    if (w2 >= 1 && w2 <= 8) {
-      W = w2;
-      C = (nchunks + 32 * W - 1) / (32 * W);
-      C += C & 1;
-      if (C < 2) C = 2;
-    }
-  }
   const int bestC = (int)C, bestW = (int)W;
   p.fast = true;
   p.C = bestC;

@@ -227,7 +227,6 @@ struct V2Args {
   int64_t ldy;
 };
 
-template <int SKIP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
     k3_v2_kernel(const __grid_constant__ CUtensorMap map_a,
                  const __grid_constant__ CUtensorMap map_b, V2Args a) {
@@ -363,10 +362,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         }
         mbar_wait(&ss->st_empty[ks], kph ^ 1);
         tc_fence_after();
-        if (SKIP != 1) {
-          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col(ks), r);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
+        tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col(ks), r);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(full_st + ks * 8);
@@ -410,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
         mbar_wait(&ss->st_empty[ks], kph ^ 1);
         uint8_t* tile = b8 + ks * V2_B8_STAGE;
 #pragma unroll
-        for (int i = 0; i < (SKIP == 2 ? 0 : 3); ++i) {
+        for (int i = 0; i < 3; ++i) {
           const int u = e + i * 128;
           const int r = u >> 2, j = u & 3;
           const uint4 v = p[i];
@@ -589,23 +586,17 @@ cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.y = a.y;
   v.ldy = a.ldy;
   const size_t smem = 1024 + V2_PS * V2_PK_STAGE + V2_KS * V2_B8_STAGE + sizeof(V2Smem);
-  static const int skip = [] {  // timing experiments only
-    const char* e = getenv("CRT_K3_SKIP");
-    const int v = e ? atoi(e) : 0;
-    return v >= 0 && v <= 2 ? v : 0;
-  }();
-  auto kern = skip == 1 ? k3_v2_kernel<1> : skip == 2 ? k3_v2_kernel<2> : k3_v2_kernel<0>;
-  static bool attr[3] = {false, false, false};
-  if (!attr[skip]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k3_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    attr[skip] = true;
+    attr = true;
   }
   const int tiles = v.mtiles * v.ntiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  kern<<<(unsigned)(2 * pairs), V2_THREADS, smem, st>>>(ma, mb, v);
+  k3_v2_kernel<<<(unsigned)(2 * pairs), V2_THREADS, smem, st>>>(ma, mb, v);
   ++*launches;
   return cudaGetLastError();
 }

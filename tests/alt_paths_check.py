@@ -1,0 +1,39 @@
+"""Parity of the opt-in kernel paths, run in a subprocess by
+tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K3_V1=1 set before the
+library loads (the switches are read once per process)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import oracle as O  # noqa: E402
+import paper_2512_03673_b200 as crt  # noqa: E402
+from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec  # noqa: E402
+
+
+def main():
+    dev = "cuda"
+    to_t = lambda b: torch.from_numpy(b.astype(np.uint16).view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
+    for n0 in (4, 16):
+        for fam in ("gaussian", "colwise", "rowwise"):
+            for (m, k, n) in ((97, 3072, 80), (40, 12288, 48)):
+                xb = O.synth_input(m, k, fam, 3 + n0)
+                wb = O.synth_input(n, k, "gaussian", 4 + n0)
+                x, w = to_t(xb), to_t(wb)
+                spec = RotationSpec(RotationKind.regular, n0)
+                codes, s32, s64 = crt.rotate_quantize(x, spec, QuantSpec(4), scales64=True)
+                layer = crt.prepare_layer(w, None, spec)
+                acc = crt.forward(x, layer, QuantSpec(4), out="i32")
+                xd, wd = O.from_bf16_bits(xb), O.from_bf16_bits(wb)
+                wc, ws = O.prepare_layer(wd, O.ROT_REGULAR, n0)
+                f = O.forward(xd, wc, ws, None, O.ROT_REGULAR, n0)
+                assert np.array_equal(codes[:, :k // 2].cpu().numpy(),
+                                      O.pack_int4_rows(f["act_codes"])), (n0, fam, m, k)
+                assert np.array_equal(s64.cpu().numpy(), f["act_scales"]), (n0, fam, m, k)
+                assert np.array_equal(acc.cpu().numpy(), f["acc"]), (n0, fam, m, k)
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,18 @@
+"""Opt-in kernel paths stay bit-exact: the tensor-core K1 (CRT_K1_MMA=1) and
+the v1 single-CTA K3 (CRT_K3_V1=1), each in a fresh process."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"CRT_K1_MMA": "1"}, {"CRT_K3_V1": "1"}])
+def test_opt_in_paths_bit_exact(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
