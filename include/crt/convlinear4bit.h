@@ -135,6 +135,18 @@ crt_status crt_layer_prepare_shard(const crt_layer_desc* desc, const void* w,
                                    int64_t ldw, const float* bias, int32_t rank,
                                    int32_t nranks, void* stream, crt_layer** out);
 
+/* f2: a layer prepared and saved by the reference
+ * (save_prepared_layer, pipeline.cpp:257-314; loaded there by
+ * load_prepared_layer, :288-314).  HOST buffers: codes in the reference
+ * layout (bits 4: pack_int4 rows of ceil(K/2) bytes, tensorio.cpp:162-171;
+ * bits 8: int8 rows), ld_codes bytes per row; fp32 per-channel scales
+ * (weights.scales.crt is f32); optional f64 bias (bias.crt).  Codes are used
+ * as given (no rotation / quantisation); INVALID_VALUE if a scale is not
+ * positive and finite (quant.cpp:31-35).  Synchronises `stream`. */
+crt_status crt_layer_from_codes(const crt_layer_desc* desc, const uint8_t* codes_host,
+                                int64_t ld_codes, const float* scales_host,
+                                const double* bias_host, void* stream, crt_layer** out);
+
 crt_status crt_layer_destroy(crt_layer* layer);
 
 /* Geometry of a prepared layer (host query). */

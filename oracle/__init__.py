@@ -430,6 +430,17 @@ class Ref:
         return out
 
     @staticmethod
+    def save_prepared_layer(path, w, bias=None, kind=ROT_REGULAR, group=16,
+                            identity_tail=False, bits=4):
+        """The reference's prepare_layer + save_prepared_layer
+        (pipeline.cpp:158-176, :257-287) into directory `path`."""
+        w = _f64(w)
+        n, k = w.shape
+        b = None if bias is None else _f64(bias)
+        _check(ref().ref_save_prepared_layer(path.encode(), _p(w), n, k, _p(b), kind, group,
+                                             int(identity_tail), bits), "ref")
+
+    @staticmethod
     def reference_forward(x, w, bias=None):
         x, w = _f64(x), _f64(w)
         b = None if bias is None else _f64(bias)

@@ -8,6 +8,7 @@ hand-written for sm_100a behind the C-ABI in include/crt/convlinear4bit.h.
 """
 from ._abi import (CapacityError, CudaError, Error, FormatError, InvalidOrderError,  # noqa: F401
                    InvalidValueError, ShapeError, UnsupportedError, load)
+from .tensorio import load_prepared_layer, read_tensor  # noqa: F401
 from .api import (PreparedLayer, QuantSpec, RotationKind, RotationSpec, Workspace,  # noqa: F401
                   forward, int_gemm, launch_count, packed_row_bytes, prepare_layer,
                   prepare_layer_shard, quant_gemm, regular, rotate_quantize,
@@ -18,5 +19,5 @@ __all__ = [
     "FormatError", "CudaError", "UnsupportedError", "RotationKind", "RotationSpec", "QuantSpec",
     "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "rotate_quantize_into", "prepare_layer",
     "prepare_layer_shard", "forward", "quant_gemm", "int_gemm", "launch_count",
-    "packed_row_bytes", "load",
+    "packed_row_bytes", "load", "load_prepared_layer", "read_tensor",
 ]

@@ -92,6 +92,8 @@ _SIGS = {
                                  ctypes.POINTER(_P)]),
     "crt_layer_prepare_shard": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _I32, _I32, _P,
                                        ctypes.POINTER(_P)]),
+    "crt_layer_from_codes": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _P, _P,
+                                    ctypes.POINTER(_P)]),
     "crt_layer_destroy": (_I32, [_P]),
     "crt_layer_info": (_I32, [_P, ctypes.POINTER(LayerDescC)]),
     "crt_layer_export": (_I32, [_P, _P, _I64, _P, _P, _P]),

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -258,6 +259,66 @@ static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t l
   }
   int64_t launches = 0;
   e = crt::k3_prepare_weights(L->codes, L->ldc, Ns, K, d->bits_w, &L->tiles, st, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "weight tiling");
+  }
+  *out = L;
+  return CRT_OK;
+}
+
+// f2: a layer prepared elsewhere (reference save_prepared_layer,
+// pipeline.cpp:257-314): codes already rotated + quantised, given on the host
+// in the reference layout (pack_int4 rows of ceil(K/2) bytes, or int8 rows),
+// per-channel fp32 scales (weights.scales.crt is f32) and an optional f64
+// bias.  No rotation or quantisation is applied.
+crt_status crt_layer_from_codes(const crt_layer_desc* d, const uint8_t* codes_host,
+                                int64_t ld_codes, const float* scales_host,
+                                const double* bias_host, void* stream, crt_layer** out) {
+  if (!d || !out || !codes_host || !scales_host) return fail(CRT_ERR_INVALID_VALUE, "null argument");
+  *out = nullptr;
+  if (d->bits_w != 4 && d->bits_w != 8) return fail(CRT_ERR_INVALID_VALUE, "bits_w must be 4 or 8");
+  const int64_t N = d->out_features, K = d->in_features;
+  if (N < 0 || K < 0) return fail(CRT_ERR_SHAPE, "negative shape");
+  const int64_t row = d->bits_w == 4 ? (K + 1) / 2 : K;
+  if (ld_codes < row) return fail(CRT_ERR_SHAPE, "ld_codes smaller than one packed row");
+  int64_t group = 1, rot_cols = K;
+  crt_status rs = resolve_rotation(&d->rotation, K, &group, &rot_cols);
+  if (rs != CRT_OK) return rs;
+  cudaStream_t st = (cudaStream_t)stream;
+  crt_layer* L = new crt_layer();
+  L->desc = *d;
+  L->n_total = N;
+  L->row_offset = 0;
+  L->ldc = d->bits_w == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
+  const size_t nalloc = (size_t)(N ? N : 1);
+  std::vector<double> s64(nalloc);
+  std::vector<float> b32(nalloc, 0.f);
+  for (int64_t n = 0; n < N; ++n) {
+    if (!(scales_host[n] > 0.f) || !std::isfinite(scales_host[n]))  // quant.cpp:31-35
+      return delete L, fail(CRT_ERR_INVALID_VALUE, "weight scale not positive and finite");
+    s64[n] = (double)scales_host[n];
+    if (bias_host) b32[n] = (float)bias_host[n];
+  }
+  cudaError_t e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
+  if (e == cudaSuccess && bias_host) e = cudaMalloc(&L->bias, 4 * nalloc);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L->codes, 0, (size_t)L->ldc * nalloc, st);
+  if (e == cudaSuccess && N && row)
+    e = cudaMemcpy2DAsync(L->codes, L->ldc, codes_host, ld_codes, row, N, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s32, scales_host, 4 * N, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s64, s64.data(), 8 * N, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && bias_host && N)
+    e = cudaMemcpyAsync(L->bias, b32.data(), 4 * N, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host staging vectors go out of scope
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "layer_from_codes");
+  }
+  int64_t launches = 0;
+  e = crt::k3_prepare_weights(L->codes, L->ldc, N, K, d->bits_w, &L->tiles, st, &launches);
   g_launches += launches;
   if (e != cudaSuccess) {
     crt_layer_destroy(L);
