@@ -108,6 +108,14 @@ crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K
                             uint8_t* codes, int64_t ld_codes, float* scales_f32,
                             double* scales_f64, void* stream);
 
+/* f4: per-row exact max |group_rotate(x)| (device, M
+ * doubles; +inf for a row with a non-finite value).  The reference's
+ * outlier_amplitude(group_rotate(x)) (analysis.cpp:12-17) is the max over
+ * rows; rotation_sweep (analysis.cpp:89-117) runs it per (kind, group). */
+crt_status crt_rotated_row_absmax(const void* x, int32_t x_dtype, int64_t M, int64_t K,
+                                  int64_t ldx, const crt_rotation_spec* rot, double* amax_rows,
+                                  void* stream);
+
 /* -------------------------------------------------------------------------
  * K2: prepare_layer -- replaces pipeline.cpp:158-176.  Rotates W (N x K,
  * device, row stride ldw elements) along K, quantizes per output channel and

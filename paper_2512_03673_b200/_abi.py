@@ -88,6 +88,8 @@ _SIGS = {
     "crt_sylvester_hadamard": (_I32, [_I32, _P]),
     "crt_rotate_quant": (_I32, [_P, _I32, _I64, _I64, _I64, ctypes.POINTER(RotationSpecC), _I32,
                                 _P, _I64, _P, _P, _P]),
+    "crt_rotated_row_absmax": (_I32, [_P, _I32, _I64, _I64, _I64, ctypes.POINTER(RotationSpecC),
+                                      _P, _P]),
     "crt_layer_prepare": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _P,
                                  ctypes.POINTER(_P)]),
     "crt_layer_prepare_shard": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _I32, _I32, _P,

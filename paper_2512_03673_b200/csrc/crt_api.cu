@@ -87,7 +87,7 @@ crt_status resolve_rotation(const crt_rotation_spec* rot, int64_t cols, int64_t*
 
 crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                   const crt_rotation_spec* rot, int32_t bits, uint8_t* codes, int64_t ldc,
-                  float* s32, double* s64, cudaStream_t st) {
+                  float* s32, double* s64, cudaStream_t st, double* amax = nullptr) {
   if (x_dtype != CRT_DTYPE_BF16 && x_dtype != CRT_DTYPE_F32)
     return fail(CRT_ERR_INVALID_VALUE, "unsupported input dtype");
   if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
@@ -122,6 +122,7 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
   a.ldc = ldc;
   a.s32 = s32;
   a.s64 = s64;
+  a.amax = amax;
   a.err = device_error_word();
   if (!a.err) return fail(CRT_ERR_CUDA, "device error word allocation failed");
   crt::K1Plan plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx,
@@ -195,6 +196,25 @@ crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K
                             void* stream) {
   return run_k1(x, x_dtype, M, K, ldx, rot, bits, codes, ld_codes, scales_f32, scales_f64,
                 (cudaStream_t)stream);
+}
+
+// f4: outlier_amplitude(group_rotate(x)) per row (analysis.cpp:12-17,
+// pipeline.cpp:111-151) -- the exact max |y_ref| K1 already settles.  The
+// codes go to a stream-ordered scratch buffer.
+crt_status crt_rotated_row_absmax(const void* x, int32_t x_dtype, int64_t M, int64_t K,
+                                  int64_t ldx, const crt_rotation_spec* rot, double* amax_rows,
+                                  void* stream) {
+  if (!amax_rows) return fail(CRT_ERR_INVALID_VALUE, "null output");
+  if (M <= 0 || K <= 0) return fail(CRT_ERR_SHAPE, "outlier_amplitude: empty matrix");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ldc = ((K + 1) / 2 + 15) / 16 * 16;
+  uint8_t* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, (size_t)ldc * M, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scratch alloc");
+  crt_status r = run_k1(x, x_dtype, M, K, ldx, rot, 4, scratch, ldc, nullptr, nullptr, st,
+                        amax_rows);
+  cudaFreeAsync(scratch, st);
+  return r;
 }
 
 crt_status crt_device_status(void* stream, int32_t reset) {

@@ -825,6 +825,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     if (w == 0 && lane == 0) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
+      if (a.amax) a.amax[row] = amax_ref;  // exact max|y_ref| (outlier analysis)
     }
     if constexpr (BULK) {
       if (W == 1) __syncwarp();
@@ -1107,6 +1108,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
     if (w == 0 && lane == 0) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
+      if (a.amax) a.amax[row] = amax_ref;  // exact max|y_ref| (outlier analysis)
     }
     if constexpr (BULK) {
       // every lane of the team is done with this stage: refill it with the
@@ -1185,6 +1187,7 @@ __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
     if (tid == 0) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
+      if (a.amax) a.amax[row] = bad ? INFINITY : m;
     }
     __syncthreads();
   }

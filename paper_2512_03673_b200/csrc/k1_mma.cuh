@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kK1MThreads, kK1MMinBlocks) k1_mma(K1Args a) {
     if (w == 0 && lane == 0) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
+      if (a.amax) a.amax[row] = amax_ref;
     }
     if (W == 1) __syncwarp();
     else named_bar_sync(1 + team, W * 32);

@@ -21,6 +21,7 @@ struct K1Args {
   int64_t ldc;
   float* s32;         // nullable
   double* s64;        // nullable
+  double* amax;       // nullable: exact per-row max |y_ref| (outlier_amplitude)
   int* err;           // device error word
 };
 
