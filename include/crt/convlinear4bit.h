@@ -179,6 +179,19 @@ crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_sc
                           int32_t bits_a, const crt_layer* layer, int64_t M,
                           int32_t out_kind, void* y, int64_t ldy, void* stream);
 
+/* W4A4 fast path (K3 v3, hardware int4 expansion): K1 with the 4-bit codes
+ * stored ONE INT8 PER CODE (values -7..7, same codes as crt_rotate_quant)
+ * plus the per-row code sums, and the GEMM that consumes them.  Device
+ * buffers; codes M x ld_codes (>= K) bytes, code_sums M int32.
+ * crt_quant_gemm_i8 needs K % 32 == 0 and 16-byte aligned rows, else
+ * UNSUPPORTED (use crt_rotate_quant + crt_quant_gemm). */
+crt_status crt_rotate_quant_i8(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
+                               const crt_rotation_spec* rot, uint8_t* codes, int64_t ld_codes,
+                               float* scales_f32, int32_t* code_sums, void* stream);
+crt_status crt_quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                             const int32_t* code_sums, const crt_layer* layer, int64_t M,
+                             int32_t out_kind, void* y, int64_t ldy, void* stream);
+
 /* -------------------------------------------------------------------------
  * a9: forward -- replaces pipeline.cpp:206-233: K1 on x, then K3 against the
  * layer.  bits_a in {4, 8} else INVALID_VALUE (:213-215); x must have

@@ -11,13 +11,14 @@ from ._abi import (CapacityError, CudaError, Error, FormatError, InvalidOrderErr
 from .tensorio import load_prepared_layer, read_tensor  # noqa: F401
 from .api import (PreparedLayer, QuantSpec, RotationKind, RotationSpec, Workspace,  # noqa: F401
                   forward, int_gemm, launch_count, packed_row_bytes, prepare_layer,
-                  prepare_layer_shard, quant_gemm, regular, rotate_quantize,
+                  prepare_layer_shard, quant_gemm, quant_gemm_i8, regular, rotate_quantize,
+                  rotate_quantize_i8,
                   rotate_quantize_into, sylvester)
 
 __all__ = [
     "Error", "InvalidOrderError", "InvalidValueError", "ShapeError", "CapacityError",
     "FormatError", "CudaError", "UnsupportedError", "RotationKind", "RotationSpec", "QuantSpec",
     "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "rotate_quantize_into", "prepare_layer",
-    "prepare_layer_shard", "forward", "quant_gemm", "int_gemm", "launch_count",
+    "prepare_layer_shard", "forward", "quant_gemm", "quant_gemm_i8", "rotate_quantize_i8", "int_gemm", "launch_count",
     "packed_row_bytes", "load", "load_prepared_layer", "read_tensor",
 ]

@@ -99,6 +99,9 @@ _SIGS = {
     "crt_layer_destroy": (_I32, [_P]),
     "crt_layer_info": (_I32, [_P, ctypes.POINTER(LayerDescC)]),
     "crt_layer_export": (_I32, [_P, _P, _I64, _P, _P, _P]),
+    "crt_rotate_quant_i8": (_I32, [_P, _I32, _I64, _I64, _I64, ctypes.POINTER(RotationSpecC), _P,
+                                   _I64, _P, _P, _P]),
+    "crt_quant_gemm_i8": (_I32, [_P, _I64, _P, _P, _P, _I64, _I32, _P, _I64, _P]),
     "crt_quant_gemm": (_I32, [_P, _I64, _P, _I32, _P, _I64, _I32, _P, _I64, _P]),
     "crt_workspace_create": (_I32, [_I64, _I64, ctypes.POINTER(_P)]),
     "crt_workspace_destroy": (_I32, [_P]),

@@ -311,6 +311,37 @@ def quant_gemm(codes: torch.Tensor, scales: torch.Tensor, layer: PreparedLayer,
     return y
 
 
+def rotate_quantize_i8(x: torch.Tensor, rotation: RotationSpec):
+    """K1 for the hardware-expansion GEMM: 4-bit codes stored one int8 per
+    code ([M, ld] uint8 holding -7..7 as int8), fp32 scales and the per-row
+    code sums (int32)."""
+    _check_2d_cuda(x, "x")
+    M, K = x.shape
+    ld = max(16, (K + 15) // 16 * 16)
+    codes = torch.empty((M, ld), dtype=torch.uint8, device=x.device)
+    s32 = torch.empty(M, dtype=torch.float32, device=x.device)
+    sums = torch.empty(M, dtype=torch.int32, device=x.device)
+    rc = rotation.c()
+    check(_lib().crt_rotate_quant_i8(_ptr(x), _dtype_code(x), M, K, x.stride(0), ctypes.byref(rc),
+                                     _ptr(codes), ld, _ptr(s32), _ptr(sums), _stream(x)))
+    return codes, s32, sums
+
+
+def quant_gemm_i8(codes: torch.Tensor, scales: torch.Tensor, sums: torch.Tensor,
+                  layer: PreparedLayer, *, out: str = "bf16",
+                  y: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """K3 v3 (weights expanded in hardware by tcgen05.cp) on rotate_quantize_i8
+    output."""
+    M = codes.shape[0]
+    N = layer.out_features
+    if y is None:
+        y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=codes.device)
+    check(_lib().crt_quant_gemm_i8(_ptr(codes), codes.stride(0), _ptr(scales), _ptr(sums),
+                                   layer.handle, M, _OUT[out], _ptr(y), y.stride(0),
+                                   _stream(codes)))
+    return y
+
+
 def int_gemm(codes: torch.Tensor, layer: PreparedLayer, aq: QuantSpec = QuantSpec(4)):
     """Raw int32 accumulators (int_gemm, pipeline.cpp:178-204) of packed
     activation codes against the prepared weights."""

@@ -87,10 +87,12 @@ crt_status resolve_rotation(const crt_rotation_spec* rot, int64_t cols, int64_t*
 
 crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                   const crt_rotation_spec* rot, int32_t bits, uint8_t* codes, int64_t ldc,
-                  float* s32, double* s64, cudaStream_t st, double* amax = nullptr) {
+                  float* s32, double* s64, cudaStream_t st, double* amax = nullptr,
+                  int32_t* rowsum = nullptr) {
+  // bits 5 (internal): 4-bit codes stored one int8 per code, + row code sums
   if (x_dtype != CRT_DTYPE_BF16 && x_dtype != CRT_DTYPE_F32)
     return fail(CRT_ERR_INVALID_VALUE, "unsupported input dtype");
-  if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
+  if (bits != 4 && bits != 8 && bits != 5) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
   if (M < 0 || K < 0) return fail(CRT_ERR_SHAPE, "negative shape");
   int64_t group = 1, rot_cols = K;
   crt_status rs = resolve_rotation(rot, K, &group, &rot_cols);
@@ -105,7 +107,7 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
     return CRT_OK;
   }
   if (ldx < K) return fail(CRT_ERR_SHAPE, "ldx < K");
-  const int64_t row_bytes = bits == 4 ? (K + 1) / 2 : K;
+  const int64_t row_bytes = bits == 4 ? (K + 1) / 2 : K;  // bits 5, 8: one byte per code
   if (ldc < row_bytes) return fail(CRT_ERR_SHAPE, "ld_codes too small for one packed row");
   if (x == nullptr || codes == nullptr) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
   const bool f32 = x_dtype == CRT_DTYPE_F32;
@@ -123,6 +125,7 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
   a.s32 = s32;
   a.s64 = s64;
   a.amax = amax;
+  a.rowsum = rowsum;
   a.err = device_error_word();
   if (!a.err) return fail(CRT_ERR_CUDA, "device error word allocation failed");
   crt::K1Plan plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx,
@@ -153,6 +156,7 @@ struct crt_workspace {
   int64_t max_m, max_k;
   uint8_t* codes;
   float* s32;
+  int32_t* rowsum;
 };
 
 extern "C" {
@@ -194,6 +198,7 @@ crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K
                             const crt_rotation_spec* rot, int32_t bits, uint8_t* codes,
                             int64_t ld_codes, float* scales_f32, double* scales_f64,
                             void* stream) {
+  if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
   return run_k1(x, x_dtype, M, K, ldx, rot, bits, codes, ld_codes, scales_f32, scales_f64,
                 (cudaStream_t)stream);
 }
@@ -396,9 +401,10 @@ crt_status crt_layer_export(const crt_layer* L, uint8_t* codes, int64_t ld_codes
 // ---------------------------------------------------------------------------
 // K3 + forward
 // ---------------------------------------------------------------------------
-crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
-                          int32_t bits_a, const crt_layer* L, int64_t M, int32_t out_kind,
-                          void* y, int64_t ldy, void* stream) {
+static crt_status quant_gemm_impl(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                                  const int32_t* a_sums, int32_t layout, int32_t bits_a,
+                                  const crt_layer* L, int64_t M, int32_t out_kind, void* y,
+                                  int64_t ldy, void* stream) {
   if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
   if (bits_a != 4 && bits_a != 8) return fail(CRT_ERR_INVALID_VALUE, "activation bits must be 4 or 8");
   if (out_kind < CRT_OUT_BF16 || out_kind > CRT_OUT_I32_ACC)
@@ -418,6 +424,8 @@ crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_sc
   crt::K3Args a{};
   a.a_codes = a_codes;
   a.lda = lda;
+  a.a_layout = layout;
+  a.a_sums = a_sums;
   a.a_scales = a_scales;
   a.w = L->tiles;
   a.w_scales = L->s32;
@@ -429,10 +437,34 @@ crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_sc
   a.out_kind = out_kind;
   a.y = y;
   a.ldy = ldy;
+  if (layout == 1 && !crt::k3_v3_supported(a))
+    return fail(CRT_ERR_UNSUPPORTED, "int8-stored activation codes need the v3 GEMM shapes");
   cudaError_t e = crt::k3_launch(a, (cudaStream_t)stream, &launches);
   g_launches += launches;
   if (e != cudaSuccess) return cuda_fail(e, "quant_gemm launch");
   return CRT_OK;
+}
+
+crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                          int32_t bits_a, const crt_layer* L, int64_t M, int32_t out_kind,
+                          void* y, int64_t ldy, void* stream) {
+  return quant_gemm_impl(a_codes, lda, a_scales, nullptr, 0, bits_a, L, M, out_kind, y, ldy,
+                         stream);
+}
+
+crt_status crt_rotate_quant_i8(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
+                               const crt_rotation_spec* rot, uint8_t* codes, int64_t ld_codes,
+                               float* scales_f32, int32_t* code_sums, void* stream) {
+  if (!code_sums) return fail(CRT_ERR_INVALID_VALUE, "null code_sums");
+  return run_k1(x, x_dtype, M, K, ldx, rot, 5, codes, ld_codes, scales_f32, nullptr,
+                (cudaStream_t)stream, nullptr, code_sums);
+}
+
+crt_status crt_quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                             const int32_t* code_sums, const crt_layer* L, int64_t M,
+                             int32_t out_kind, void* y, int64_t ldy, void* stream) {
+  if (!code_sums) return fail(CRT_ERR_INVALID_VALUE, "null code_sums");
+  return quant_gemm_impl(a_codes, lda, a_scales, code_sums, 1, 4, L, M, out_kind, y, ldy, stream);
 }
 
 crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** out) {
@@ -444,8 +476,10 @@ crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** ou
   const int64_t ld = (max_k + 15) / 16 * 16;  // room for int8 codes too
   cudaError_t e = cudaMalloc(&w->codes, (size_t)ld * (max_m ? max_m : 1));
   if (e == cudaSuccess) e = cudaMalloc(&w->s32, 4 * (size_t)(max_m ? max_m : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&w->rowsum, 4 * (size_t)(max_m ? max_m : 1));
   if (e != cudaSuccess) {
     cudaFree(w->codes);
+    cudaFree(w->s32);
     delete w;
     return cuda_fail(e, "workspace alloc");
   }
@@ -457,6 +491,7 @@ crt_status crt_workspace_destroy(crt_workspace* w) {
   if (!w) return CRT_OK;
   cudaFree(w->codes);
   cudaFree(w->s32);
+  cudaFree(w->rowsum);
   delete w;
   return CRT_OK;
 }
@@ -469,6 +504,15 @@ crt_status crt_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64
   if (bits_a != 4 && bits_a != 8)  // pipeline.cpp:213-215
     return fail(CRT_ERR_INVALID_VALUE, "forward: activation bits must be 4 or 8");
   if (M > ws->max_m || K > ws->max_k) return fail(CRT_ERR_SHAPE, "workspace too small");
+  if (bits_a == 4 && L->desc.bits_w == 4 && L->tiles.codes_ob && M > 0) {
+    // v3: int8-stored codes + code sums -> hardware-expanded weights GEMM
+    const int64_t ldc = (K + 15) / 16 * 16;
+    crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, 5, ws->codes, ldc, ws->s32,
+                          nullptr, (cudaStream_t)stream, nullptr, ws->rowsum);
+    if (s != CRT_OK) return s;
+    return quant_gemm_impl(ws->codes, ldc, ws->s32, ws->rowsum, 1, 4, L, M, out_kind, y, ldy,
+                           stream);
+  }
   const int64_t ldc = bits_a == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
   crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, bits_a, ws->codes, ldc, ws->s32,
                         nullptr, (cudaStream_t)stream);

@@ -220,6 +220,7 @@ __device__ __forceinline__ double warp_max_d(double v) {
 struct TeamScratch {
   float f[32];
   double d[32];
+  int i[32];
 };
 
 // Team of W warps (contiguous warps team*W .. team*W+W-1).  Two barriers
@@ -245,6 +246,36 @@ __device__ __forceinline__ double team_max_d(double v, TeamScratch* ts, int team
   named_bar_sync(1 + team, W * 32);
   double r = ts->d[team * W];
   for (int i = 1; i < W; ++i) r = fmax(r, ts->d[team * W + i]);
+  named_bar_sync(1 + team, W * 32);
+  return r;
+}
+
+
+// Sum of the int8 codes of row `crow` (K bytes) over the team, after the
+// team's stores are visible (called past the end-of-row barrier): each lane
+// sums 16-byte pieces with DP4A.  The K3 v3 epilogue needs it to remove the
+// offset of the decompressed weights (k3_gemm_v3.cu).
+__device__ __forceinline__ int team_code_sum(const uint8_t* crow, int64_t K, int W, int w,
+                                             TeamScratch* ts, int team) {
+  const int lane = threadIdx.x & 31;
+  int acc = 0;
+  for (int64_t off = ((int64_t)w * 32 + lane) * 16; off < K; off += (int64_t)W * 32 * 16) {
+    if (off + 16 <= K) {
+      const uint4 v = *reinterpret_cast<const uint4*>(crow + off);
+      acc = __dp4a((int)v.x, 0x01010101, acc);
+      acc = __dp4a((int)v.y, 0x01010101, acc);
+      acc = __dp4a((int)v.z, 0x01010101, acc);
+      acc = __dp4a((int)v.w, 0x01010101, acc);
+    } else {
+      for (int64_t j = off; j < K; ++j) acc += (int)(int8_t)crow[j];
+    }
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if (W == 1) return acc;
+  if (lane == 0) ts->i[team * W + w] = acc;
+  named_bar_sync(1 + team, W * 32);
+  int r = 0;
+  for (int i = 0; i < W; ++i) r += ts->i[team * W + i];
   named_bar_sync(1 + team, W * 32);
   return r;
 }
@@ -380,7 +411,7 @@ template <bool F32, int BITS>
 __device__ __noinline__ void k1_redecide(uint32_t m, const void* rowp, uint8_t* crow,
                                          int64_t c0, int64_t cstride, int64_t nchunks, double s,
                                          int64_t group, int kind, int64_t rot_cols) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   const int lane = threadIdx.x & 31;
   for (;;) {
     const uint32_t bal = __ballot_sync(0xffffffffu, m != 0);
@@ -478,7 +509,7 @@ template <bool F32, int BITS>
 __device__ __noinline__ void k1_slow_row_codes(const void* rowp, uint8_t* crow, int C, int W,
                                                int w, int64_t nchunks, bool invalid, double s,
                                                int64_t group, int kind, int64_t rot_cols) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   const int lane = threadIdx.x & 31;
   for (int c = 0; c < C; ++c) {
     const int64_t chunk = ((int64_t)c * W + w) * 32 + lane;
@@ -547,9 +578,11 @@ __device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], ui
     } else {
       uint32_t wds[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q) {
         wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                              __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040), 0x5410);
+        if constexpr (BITS == 5) wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+      }
       *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
     }
   }
@@ -576,7 +609,7 @@ __device__ __noinline__ void k1_redecide_lane(uint32_t m, const float2* vl, cons
                                               uint8_t* crow, int64_t c0, int64_t cstride,
                                               int64_t nchunks, double s, int64_t group, int kind,
                                               int64_t rot_cols) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   while (m) {
     const int bit = __ffs(m) - 1;
     m &= m - 1;
@@ -645,7 +678,7 @@ constexpr int kK1MinBlocks = 3;  // rolled kernel: <= 85 registers, 24 warps per
 template <int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) {
   constexpr int L = Stages<N0>::L;
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   __shared__ TeamScratch ts;
   __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
   extern __shared__ __align__(128) uint8_t k1_ring[];
@@ -780,7 +813,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       const float margin = (float)B * (inv * 1.05f) +
                            (float)(QMAX + 4) * 2.384185791015625e-7f + 1e-9f;
       const float thr = 0.5f - margin;
-      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
+      const float mg = __uint_as_float(kMagic23 + (BITS == 8 ? 0u : 8u));
       const float2 iv = make_float2(inv, inv);
       const float2 cc = make_float2(mg, mg);
 #pragma unroll 1
@@ -830,6 +863,10 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     if constexpr (BULK) {
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
+      if (a.rowsum) {
+        const int sum = team_code_sum(crow, a.K, W, w, &ts, team);
+        if (leader) a.rowsum[row] = sum;
+      }
       if (leader) {
         const int64_t r = row + (int64_t)S * row_step;
         if (r < a.M) {
@@ -859,7 +896,7 @@ template <int C, int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) {
   constexpr int P = C / 2;
   constexpr int L = Stages<N0>::L;
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   __shared__ TeamScratch ts;
   __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
   extern __shared__ __align__(128) uint8_t k1_ring[];
@@ -1031,7 +1068,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
       // code + 8 in [1, 15] with nothing above it: one IMAD packs a byte
       // (odd*16 + even) in offset binary and one XOR 0x88888888 per word
       // turns it into two's-complement nibbles.
-      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
+      const float mg = __uint_as_float(kMagic23 + (BITS == 8 ? 0u : 8u));
       const float2 iv = make_float2(inv, inv);
       const float2 cc = make_float2(mg, mg);
 #pragma unroll
@@ -1066,10 +1103,12 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
           } else {
             uint32_t wds[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 4; ++q) {
               wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                                    __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
                                    0x5410);
+              if constexpr (BITS == 5) wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+            }
             *reinterpret_cast<uint4*>(crow + chunk * 16) =
                 make_uint4(wds[0], wds[1], wds[2], wds[3]);
           }
@@ -1115,6 +1154,10 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
       // row `stages` ahead.
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
+      if (a.rowsum) {
+        const int sum = team_code_sum(crow, a.K, W, w, &ts, team);
+        if (leader) a.rowsum[row] = sum;
+      }
       if (leader) {
         const int64_t r = row + (int64_t)S * row_step;
         if (r < a.M) {
@@ -1137,7 +1180,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
 // ---------------------------------------------------------------------------
 template <bool F32, int BITS>
 __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   extern __shared__ int8_t scodes[];
   __shared__ double red[8];
   __shared__ int redbad[8];
@@ -1188,6 +1231,11 @@ __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
       if (a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
       if (a.amax) a.amax[row] = bad ? INFINITY : m;
+      if (a.rowsum) {
+        int sum = 0;
+        for (int64_t j = 0; j < a.K; ++j) sum += scodes[j];
+        a.rowsum[row] = sum;
+      }
     }
     __syncthreads();
   }
@@ -1313,7 +1361,7 @@ cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
   // Multi-warp rows: the rolled kernel's occupancy (24 warps/SM) beats the
   // register-resident one (measured: K=12288 N0=16 67.6 vs 77.8 us); one
   // warp per row (K <= 3072): the single-pass kernel (24.6 vs 28.8 us).
-  if constexpr (!F32 && (N0 == 4 || N0 == 16)) {
+  if constexpr (!F32 && (N0 == 4 || N0 == 16) && BITS != 5) {
     if (mma_path_ok(a, N0, F32)) {
       const cudaError_t e = launch_mma<N0, BITS>(a, st, l);
       if (e != cudaErrorInvalidValue) return e;

@@ -144,7 +144,7 @@ constexpr int kK1MMinBlocks = 3;
 
 template <int N0, int BITS>
 __global__ void __launch_bounds__(kK1MThreads, kK1MMinBlocks) k1_mma(K1Args a) {
-  constexpr int QMAX = BITS == 4 ? 7 : 127;
+  constexpr int QMAX = BITS == 8 ? 127 : 7;
   __shared__ TeamScratch ts;
   __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
   extern __shared__ __align__(128) uint8_t k1_ring[];

@@ -66,14 +66,19 @@ cudaError_t launch_k1(const K1Args& a, const K1Plan& p, bool f32, int bits, cuda
     b.chunks = p.C;
     const int n0 = a.kind == kRotNone ? 1 : (int)a.group;
     if (f32) {
-      return bits == 4 ? k1_dispatch<true, 4>(b, n0, st, launches)
-                       : k1_dispatch<true, 8>(b, n0, st, launches);
+      return bits == 4   ? k1_dispatch<true, 4>(b, n0, st, launches)
+             : bits == 5 ? k1_dispatch<true, 5>(b, n0, st, launches)
+                         : k1_dispatch<true, 8>(b, n0, st, launches);
     }
-    return bits == 4 ? k1_dispatch<false, 4>(b, n0, st, launches)
-                     : k1_dispatch<false, 8>(b, n0, st, launches);
+    return bits == 4   ? k1_dispatch<false, 4>(b, n0, st, launches)
+           : bits == 5 ? k1_dispatch<false, 5>(b, n0, st, launches)
+                       : k1_dispatch<false, 8>(b, n0, st, launches);
   }
-  cudaError_t e = f32 ? (bits == 4 ? k1_exact_launch<true, 4>(a, st) : k1_exact_launch<true, 8>(a, st))
-                      : (bits == 4 ? k1_exact_launch<false, 4>(a, st) : k1_exact_launch<false, 8>(a, st));
+  cudaError_t e =
+      f32 ? (bits == 4 ? k1_exact_launch<true, 4>(a, st)
+             : bits == 5 ? k1_exact_launch<true, 5>(a, st) : k1_exact_launch<true, 8>(a, st))
+          : (bits == 4 ? k1_exact_launch<false, 4>(a, st)
+             : bits == 5 ? k1_exact_launch<false, 5>(a, st) : k1_exact_launch<false, 8>(a, st));
   ++*launches;
   return e;
 }

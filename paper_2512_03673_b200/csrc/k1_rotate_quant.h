@@ -22,6 +22,7 @@ struct K1Args {
   float* s32;         // nullable
   double* s64;        // nullable
   double* amax;       // nullable: exact per-row max |y_ref| (outlier_amplitude)
+  int32_t* rowsum;    // nullable: per-row sum of the int8 codes (bits 5 layout)
   int* err;           // device error word
 };
 

@@ -340,25 +340,55 @@ __global__ void k3_generic_kernel(K3Args a) {
 
 }  // namespace
 
+__global__ void k3_offset_binary_kernel(const uint8_t* src, int64_t lds, int64_t row_bytes,
+                                        uint8_t* dst, int64_t ldd, int64_t n) {
+  // two's-complement nibble <-> offset binary: flip bit 3; pad = code 0
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ldd, c = i - r * ldd;
+    dst[i] = c < row_bytes ? src[r * lds + c] ^ 0x88 : 0x88;
+  }
+}
+
 cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int64_t K, int bits,
                                K3Weights* out, cudaStream_t st, int64_t* launches) {
-  (void)st;
-  (void)launches;
   out->codes = codes;
+  out->codes_ob = nullptr;
+  out->ld_ob = 0;
   out->ld = ldc;
   out->N = N;
   out->K = K;
   out->bits = bits;
-  return cudaSuccess;
+  if (bits != 4 || N == 0) return cudaSuccess;
+  // v3 operand: offset-binary copy (TMA 16U4 + tcgen05.cp decompress -> 4*(w+8))
+  uint8_t* ob = nullptr;
+  const int64_t ldo = (K + 127) / 128 * 64;
+  cudaError_t e = cudaMalloc(&ob, (size_t)ldo * N);
+  if (e != cudaSuccess) return e;
+  const int64_t n = ldo * N;
+  k3_offset_binary_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(
+      codes, ldc, (K + 1) / 2, ob, ldo, n);
+  out->ld_ob = ldo;
+  ++*launches;
+  out->codes_ob = ob;
+  return cudaGetLastError();
 }
 
-void k3_free_weights(K3Weights* w) { w->codes = nullptr; }
+void k3_free_weights(K3Weights* w) {
+  cudaFree(const_cast<uint8_t*>(w->codes_ob));
+  w->codes_ob = nullptr;
+  w->codes = nullptr;
+}
 
 cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   static const bool force_v1 = [] {
     const char* e = getenv("CRT_K3_V1");
     return e && e[0] == '1';
   }();
+  if (a.a_layout == 1) {  // int8-stored 4-bit activation codes: v3 only
+    if (k3_v3_supported(a)) return k3_v3_launch(a, st, launches);
+    return cudaErrorInvalidValue;
+  }
   if (!force_v1 && k3_v2_supported(a)) return k3_v2_launch(a, st, launches);
   const bool b4 = a.bits == 4;
   const bool aligned = ((uintptr_t)a.a_codes % 16 == 0) && (a.lda % 16 == 0) &&

@@ -12,6 +12,8 @@ namespace crt {
 // 16-byte vector (the unit K3 stages).
 struct K3Weights {
   const uint8_t* codes;
+  const uint8_t* codes_ob;  // same codes in offset binary (nibble = code + 8), v3 / owned
+  int64_t ld_ob;            // its row pitch: K rounded up to 128 codes (64 B; TMA 16U4 needs it)
   int64_t ld;
   int64_t N;
   int64_t K;
@@ -21,6 +23,8 @@ struct K3Weights {
 struct K3Args {
   const uint8_t* a_codes;  // M x lda bytes
   int64_t lda;
+  int32_t a_layout;        // 0: packed like pack_int4 (bits 4) / int8 (bits 8); 1: int8 per 4-bit code
+  const int32_t* a_sums;   // layout 1: per-row sum of the codes (K1 rowsum)
   const float* a_scales;   // M
   K3Weights w;             // by value (device pointers inside)
   const float* w_scales;   // N
@@ -40,6 +44,10 @@ cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 // v2: persistent 2-SM (cta_group::2) kernel, TMA-staged packed tiles, A
 // expanded into TMEM (k3_gemm_v2.cu).  W4A4 only.
 bool k3_v2_supported(const K3Args& a);
+// v3: hardware int4 expansion (tcgen05.cp decompress) of offset-binary
+// weights into TMEM, int8 activation codes as the smem operand (k3_gemm_v3.cu).
+bool k3_v3_supported(const K3Args& a);
+cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 
 }  // namespace crt

@@ -1,0 +1,490 @@
+// k3_gemm_v3.cu -- K3 v3: W4A4 GEMM with HARDWARE int4 -> int8 expansion.
+//
+// Replaces int_gemm (pipeline.cpp:178-204) and the dequant loop of forward
+// (pipeline.cpp:224-230).  Same 2-SM tcgen05 kind::i8 machinery as v2, with
+// the operands swapped so that no thread touches an operand byte:
+//   * A = the prepared WEIGHTS, stored packed in offset binary (nibble =
+//     code + 8).  TMA (CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 128B swizzle)
+//     stages them as padded 4-bit units; the MMA thread expands them with
+//     tcgen05.cp ... .b8x16.b4x16_p64 straight into TMEM (measured on B200,
+//     tools/probes/tcgen05_cp_probe.cu: byte = nibble << 2), i.e. the A
+//     operand holds 4*(w + 8).
+//   * B = the ACTIVATION codes from K1 stored one int8 per code (values
+//     -7..7); TMA puts them directly into the 128B-swizzled K-major smem
+//     operand layout.
+//   * D = W * X^T in TMEM (lane = output channel, column = token):
+//     acc' = 4*sum(w*a) + 32*S_a[m], S_a = per-token code sum from K1, so
+//     acc = (acc' - 32*S_a[m]) >> 2 exactly (|acc'| < 2^31 for K <= 1,277,000).
+// Pair tile: 256 channels (128 per CTA, A from its own TMEM) x 192 tokens
+// (96 token rows of B per CTA).  Persistent over tiles; warp roles: 0 TMA
+// producer, 1 MMA issuer, 3 decompress issuer (a separate tcgen05 issuing
+// thread, so the smem->TMEM expansion runs beside the MMAs instead of in
+// their in-order queue: fc2 2105 -> 2693 TOPS), 4..11 epilogue.  The
+// accumulators are double buffered so the epilogue (TMEM -> dequant ->
+// direct coalesced stores, lane = channel) overlaps the next tile's MMAs.
+// TMEM per CTA (512 columns): acc0 [0,192), A slots 0,1 [192,256), acc1
+// [256,448), A slots 2,3 [448,512); one slot = one 128-code K block.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "k3_gemm.h"
+
+namespace crt {
+namespace {
+
+constexpr int V3_BM = 128;         // channels per CTA (pair: 256)
+constexpr int V3_BT = 192;         // tokens per pair tile
+constexpr int V3_BTH = V3_BT / 2;  // token rows of B per CTA
+constexpr int V3_PS = 7;           // smem stages
+constexpr int V3_THREADS = 384;
+constexpr int V3_A_STAGE = V3_BM * 128;  // 16 KB: 128 rows x (8 x 16 B padded units)
+constexpr int V3_B_STAGE = V3_BTH * 128; // 12 KB int8
+constexpr int V3_STAGE = V3_A_STAGE + V3_B_STAGE;
+// transaction bytes of one stage: a 16U4_ALIGN16B box completes its PACKED
+// data bytes (64 per row), not its padded smem footprint (128 per row) --
+// measured, tools/probes/tma_u4_probe.cu
+constexpr int V3_STAGE_TX = V3_BM * 64 + V3_B_STAGE;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the pair bit: CTA 0's barrier
+
+struct V3Smem {
+  uint64_t full[V3_PS];   // leader: 2 arrivals (one per CTA) + tx bytes of both CTAs
+  uint64_t empty[V3_PS];  // both: MMA commit multicast
+  uint64_t acc_full[2];   // both: MMA commit multicast
+  uint64_t acc_empty[2];  // leader: 8 epilogue warps x 2 CTAs
+  uint64_t dec_full[4];   // leader: decompress warp's commit (A slot expanded)
+  uint64_t dec_empty[4];  // leader: MMA commit (A slot consumed)
+  uint32_t tmem_base;
+  float sa[2][V3_BT];     // per-token activation scale of the tile
+  int sums[2][V3_BT];     // per-token code sums
+};
+
+__device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
+__device__ __forceinline__ uint32_t a_col(int s) {
+  return (s < 2 ? 192u : 448u) + (uint32_t)(s & 1) * 32u;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// commit to the leader CTA's barrier only
+__device__ __forceinline__ void tc_commit_leader(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// 128B-swizzled K-major shared-memory descriptor (8-row groups 1024 B apart)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+// TMA 2-D load that completes on the LEADER CTA's barrier (2-SM form).
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, int x, int y,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerMask)
+      : "memory");
+}
+// smem padded int4 (16 nibbles + 64-bit pad per 16 B unit) -> TMEM int8
+// containers (nibble << 2), 128 lanes x 32 codes, both CTAs of the pair.
+__device__ __forceinline__ void tc_cp_decompress(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b.b8x16.b4x16_p64 [%0], %1;" ::"r"(taddr),
+               "l"(sdesc)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct V3Args {
+  int64_t M, N, K;
+  int32_t ttiles, ctiles;  // token tiles (192), channel tiles (256)
+  const float* a_scales;
+  const int32_t* a_sums;
+  const float* w_scales;
+  const float* bias;
+  int32_t out_kind;  // 0 bf16, 1 f32, 2 int32 accumulators
+  void* y;
+  int64_t ldy;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
+    k3_v3_kernel(const __grid_constant__ CUtensorMap map_w,
+                 const __grid_constant__ CUtensorMap map_x, V3Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* stg = smem;                                        // V3_PS x (A 16 KB | B 12 KB)
+  V3Smem* ss = reinterpret_cast<V3Smem*>(smem + V3_PS * V3_STAGE);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int npairs = gridDim.x >> 1;
+  const int pair = blockIdx.x >> 1;
+  const int ntiles = a.ttiles * a.ctiles;
+  const int KB = (int)((a.K + 127) / 128);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < V3_PS; ++s) {
+      mbar_init(&ss->full[s], 2);
+      mbar_init(&ss->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ss->acc_full[b], 1);
+      mbar_init(&ss->acc_empty[b], 16);
+    }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&ss->dec_full[b], 1);
+      mbar_init(&ss->dec_empty[b], 1);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&ss->tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = ss->tmem_base;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs; completions land on the leader) ========
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+      const uint32_t full0 = mapa(smem_u32(&ss->full[0]), 0);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        const int tt = t % a.ttiles, ct = t / a.ttiles;
+        const int n0 = ct * 2 * V3_BM + (int)rank * V3_BM;   // this CTA's channels
+        const int m0 = tt * V3_BT + (int)rank * V3_BTH;      // this CTA's token rows
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&ss->empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&ss->full[s], 2 * V3_STAGE_TX);
+          else arrive_cluster(full0 + s * 8);
+          uint8_t* st = stg + s * V3_STAGE;
+          tma_load_2sm(st, &map_w, kb * 128, n0, &ss->full[s]);
+          tma_load_2sm(st + V3_A_STAGE, &map_x, kb * 128, m0, &ss->full[s]);
+          if (++s == V3_PS) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader) ===============================================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(2 * V3_BM, V3_BT);
+      int s = 0, slot = 0;
+      uint32_t ph = 0, sph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        mbar_wait(&ss->acc_empty[ab], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + acc_col(ab);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&ss->dec_full[slot], sph);  // A expanded (implies the stage landed)
+          tc_fence_after();
+          const uint32_t bbase = smem_u32(stg + s * V3_STAGE) + V3_A_STAGE;
+          const uint32_t acol = tmem + a_col(slot);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_pair_ts(dcol, acol + kk * 8, sw128_desc(bbase + kk * 32), idesc,
+                           (kb | kk) != 0 ? 1u : 0u);
+          tc_commit_pair(&ss->empty[s]);
+          tc_commit_leader(&ss->dec_empty[slot]);
+          if (++s == V3_PS) {
+            s = 0;
+            ph ^= 1;
+          }
+          if (++slot == 4) {
+            slot = 0;
+            sph ^= 1;
+          }
+        }
+        tc_commit_pair(&ss->acc_full[ab]);
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ===== decompress issuer (leader): padded int4 smem -> int8 TMEM ========
+    // A separate issuing thread, so the copies can run beside the MMAs.
+    if (leader && lane == 0) {
+      int s = 0, slot = 0;
+      uint32_t ph = 0, sph = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&ss->full[s], ph);
+          mbar_wait(&ss->dec_empty[slot], sph ^ 1);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(stg + s * V3_STAGE);
+          const uint32_t acol = tmem + a_col(slot);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tc_cp_decompress(acol + kk * 8, sw128_desc(abase + kk * 32));
+          tc_commit_leader(&ss->dec_full[slot]);
+          if (++s == V3_PS) {
+            s = 0;
+            ph ^= 1;
+          }
+          if (++slot == 4) {
+            slot = 0;
+            sph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM -> dequant -> direct stores =======================
+    // Lane = output channel, so for each token the warp's 32 lanes write 32
+    // consecutive channels (64 B bf16 / 128 B f32): coalesced without a
+    // transpose.  Two warps per TMEM lane quarter split the token chunks.
+    const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int et = threadIdx.x - 128;  // 0..255
+    const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      const int tt = t % a.ttiles, ct = t / a.ttiles;
+      const int64_t mb = (int64_t)tt * V3_BT;                                // tile tokens
+      const int64_t n = (int64_t)ct * 2 * V3_BM + (int64_t)rank * V3_BM + q * 32 + lane;
+      const bool nok = n < a.N;
+      const float sw = nok ? a.w_scales[n] : 0.f;
+      const float bn = (a.bias && nok) ? a.bias[n] : 0.f;
+      for (int i = et; i < V3_BT; i += 256) {
+        const int64_t m = mb + i;
+        ss->sa[ab][i] = m < a.M ? a.a_scales[m] : 0.f;
+        ss->sums[ab][i] = m < a.M ? 32 * a.a_sums[m] : 0;
+      }
+      named_bar_sync(1, 256);
+      wait_sleep(&ss->acc_full[ab], aph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = h; c < V3_BT / 32; c += 2) {
+        uint32_t acc[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32, acc);
+        const int64_t m0 = mb + c * 32;  // tokens m0 .. m0+31 of this chunk
+        if (m0 >= a.M || !nok) continue;
+        const int jn = a.M - m0 < 32 ? (int)(a.M - m0) : 32;
+        const int* sm = &ss->sums[ab][c * 32];
+        const float* sa = &ss->sa[ab][c * 32];
+        if (a.out_kind == 0) {
+          __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(a.y) + m0 * a.ldy + n;
+          if (jn == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int v = ((int)acc[j] - sm[j]) >> 2;
+              yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < jn) {
+                const int v = ((int)acc[j] - sm[j]) >> 2;
+                yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
+              }
+          }
+        } else {
+          uint32_t* yp = reinterpret_cast<uint32_t*>(a.y) + m0 * a.ldy + n;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < jn) {
+              const int v = ((int)acc[j] - sm[j]) >> 2;
+              yp[j * a.ldy] = a.out_kind == 2 ? (uint32_t)v
+                                              : __float_as_uint(fmaf((float)v * sa[j], sw, bn));
+            }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cluster(empty_acc + ab * 8);
+      if (++ab == 2) {
+        ab = 0;
+        aph ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_v3() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool k3_v3_supported(const K3Args& a) {
+  if (a.bits != 4 || a.a_layout != 1 || !a.a_sums || !a.w.codes_ob) return false;
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.K > 1277000) return false;
+  if ((uintptr_t)a.a_codes % 16 || a.lda % 16 || (uintptr_t)a.w.codes_ob % 16 || a.w.ld_ob % 64)
+    return false;
+  return encode_fn_v3() != nullptr;
+}
+
+cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  auto fn = encode_fn_v3();
+  CUtensorMap mw, mx;
+  {  // weights: N rows x K 4-bit codes (offset binary), padded 16-code units
+    cuuint64_t dims[2] = {(cuuint64_t)(a.w.ld_ob * 2), (cuuint64_t)a.N};
+    cuuint64_t strides[1] = {(cuuint64_t)a.w.ld_ob};
+    cuuint32_t box[2] = {128, (cuuint32_t)V3_BM};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&mw, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2, const_cast<uint8_t*>(a.w.codes_ob),
+           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {  // activations: M rows x K int8 codes
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)a.lda};
+    cuuint32_t box[2] = {128, (cuuint32_t)V3_BTH};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&mx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.a_codes), dims, strides,
+           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  V3Args v{};
+  v.M = a.M;
+  v.N = a.N;
+  v.K = a.K;
+  v.ttiles = (int32_t)((a.M + V3_BT - 1) / V3_BT);
+  v.ctiles = (int32_t)((a.N + 2 * V3_BM - 1) / (2 * V3_BM));
+  v.a_scales = a.a_scales;
+  v.a_sums = a.a_sums;
+  v.w_scales = a.w_scales;
+  v.bias = a.bias;
+  v.out_kind = a.out_kind;
+  v.y = a.y;
+  v.ldy = a.ldy;
+  const size_t smem = 1024 + V3_PS * V3_STAGE + sizeof(V3Smem);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k3_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = v.ttiles * v.ctiles;
+  int pairs = num_sms / 2;
+  if (pairs > tiles) pairs = tiles;
+  k3_v3_kernel<<<(unsigned)(2 * pairs), V3_THREADS, smem, st>>>(mw, mx, v);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace crt

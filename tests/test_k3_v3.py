@@ -1,0 +1,69 @@
+"""K3 v3 (weights expanded by tcgen05.cp decompression, int8 activation codes
+from K1's bits-5 mode) against the exact integer GEMM of the same codes and
+against the packed v2 path.  The int_gemm accumulators must be bit-exact
+(pipeline.cpp:178-204) and the dequantised outputs identical to v2's, which
+tests/test_gpu_parity.py pins to the oracle.  Shapes cover ragged token tiles
+(M not a multiple of 192), ragged channel tiles (N not a multiple of 256),
+partial 128-code K blocks (K % 128 != 0, K % 32 != 0) and the FLUX shapes."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _unpack(c, k):
+    c = c[:, : (k + 1) // 2].to(torch.int32)
+    lo, hi = c & 0xF, (c >> 4) & 0xF
+    lo = torch.where(lo >= 8, lo - 16, lo)
+    hi = torch.where(hi >= 8, hi - 16, hi)
+    return torch.stack([lo, hi], dim=2).reshape(c.shape[0], -1)[:, :k]
+
+
+SHAPES = [(1, 32, 16), (5, 96, 40), (7, 40, 24), (65, 100, 300), (193, 160, 257),
+          (384, 3072, 768), (257, 3104, 1000), (1024, 12288, 512), (4096, 3072, 3072)]
+
+
+@pytest.mark.parametrize("M,K,N", SHAPES)
+@pytest.mark.parametrize("n0", [4, 16])
+def test_v3_accumulators_exact(M, K, N, n0):
+    import paper_2512_03673_b200 as crt
+    from paper_2512_03673_b200 import RotationKind, RotationSpec
+    if K % n0:
+        pytest.skip("K not a multiple of the rotation group")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + K + N)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    x[0, :: max(1, K // 5)] *= 40  # outlier columns
+    w = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    spec = RotationSpec(RotationKind.regular, n0)
+    layer = crt.prepare_layer(w, torch.randn(N, device="cuda", generator=g), spec)
+    codes_p, sa = crt.rotate_quantize(x, spec)
+    codes8, sa8, sums = crt.rotate_quantize_i8(x, spec)
+    A = _unpack(codes_p, K)
+    a8 = codes8[:, :K].view(torch.int8).to(torch.int32)
+    assert torch.equal(A, a8), "int8 codes differ from the packed codes"
+    assert torch.equal(sa, sa8)
+    assert torch.equal(A.sum(1), sums)
+    B = _unpack(layer.export(scales64=False)[0], K)
+    ref = (A.double() @ B.double().T).round().to(torch.int64)
+    acc = crt.quant_gemm_i8(codes8, sa8, sums, layer, out="i32").to(torch.int64)
+    assert torch.equal(acc, ref)
+    for out in ("f32", "bf16"):
+        y2 = crt.quant_gemm(codes_p, sa, layer, out=out)
+        y3 = crt.quant_gemm_i8(codes8, sa8, sums, layer, out=out)
+        assert torch.equal(y2, y3), out
+
+
+@pytest.mark.parametrize("M,K,N", [(8, 64, 16), (193, 160, 257), (33, 48, 70), (4608, 3072, 12288)])
+def test_forward_v3_equals_packed_path(M, K, N):
+    """crt_forward routes W4A4 through K1 bits-5 + v3; its
+    output must equal K1 bits-4 + the packed GEMM."""
+    import paper_2512_03673_b200 as crt
+    from paper_2512_03673_b200 import RotationKind, RotationSpec
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    spec = RotationSpec(RotationKind.regular, 16)
+    layer = crt.prepare_layer(w, torch.randn(N, device="cuda", generator=g), spec)
+    codes_p, sa = crt.rotate_quantize(x, spec)
+    for out in ("i32", "f32", "bf16"):
+        assert torch.equal(crt.forward(x, layer, out=out), crt.quant_gemm(codes_p, sa, layer, out=out))
