@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--path", choices=["v3", "v2"], default="v3",
+                    help="K1+K3 pair: v3 (int8 codes, hardware weight expansion; what "
+                         "forward() runs) or v2 (packed codes, software expansion)")
     ap.add_argument("--parallel", choices=["replica", "column"], default="replica",
                     help="N>1: independent prompt replicas (weak scaling, default) or "
                          "column-parallel fc1/fc2 with an NCCL all-gather (strong scaling)")
@@ -240,12 +243,20 @@ def run_ours(args):
     n1, n2 = fc1.out_features, fc2.out_features  # per-rank columns
 
     # preallocated device buffers (no allocation in the timed region)
-    ld1 = (D_MODEL // 2 + 15) // 16 * 16
-    ld2 = (D_FF // 2 + 15) // 16 * 16
+    # v3 (production forward): K1 writes one int8 per 4-bit code + per-row
+    # code sums, K3 v3 expands the packed weights in hardware.  v2: K1 packs
+    # two codes per byte, K3 v2 expands in software.
+    v3 = args.path == "v3"
+    cpb = 1.0 if v3 else 0.5  # activation code bytes per element
+    ld1 = (int(D_MODEL * cpb) + 15) // 16 * 16
+    ld2 = (int(D_FF * cpb) + 15) // 16 * 16
     c1 = torch.empty(M_TOK, ld1, dtype=torch.uint8, device=dev)
     c2 = torch.empty(M_TOK, ld2, dtype=torch.uint8, device=dev)
     s1 = torch.empty(M_TOK, dtype=torch.float32, device=dev)
     s2 = torch.empty(M_TOK, dtype=torch.float32, device=dev)
+    r1 = torch.empty(M_TOK, dtype=torch.int32, device=dev)
+    r2 = torch.empty(M_TOK, dtype=torch.int32, device=dev)
+    rsum = {c1.data_ptr(): r1, c2.data_ptr(): r2}
     y1 = torch.empty(M_TOK, D_FF, dtype=torch.bfloat16, device=dev)
     y2 = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16, device=dev)
     if column:
@@ -261,12 +272,21 @@ def run_ours(args):
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def k1(xin, codes, sc, K, ld):
-        _abi.check(lib.crt_rotate_quant(P(xin), _abi.CRT_DTYPE_BF16, M_TOK, K, K, ctypes.byref(rc),
-                                        4, P(codes), ld, P(sc), None, sp))
+        if v3:
+            _abi.check(lib.crt_rotate_quant_i8(P(xin), _abi.CRT_DTYPE_BF16, M_TOK, K, K,
+                                               ctypes.byref(rc), P(codes), ld, P(sc),
+                                               P(rsum[codes.data_ptr()]), sp))
+        else:
+            _abi.check(lib.crt_rotate_quant(P(xin), _abi.CRT_DTYPE_BF16, M_TOK, K, K,
+                                            ctypes.byref(rc), 4, P(codes), ld, P(sc), None, sp))
 
     def k3(codes, ld, sc, layer, y, N):
-        _abi.check(lib.crt_quant_gemm(P(codes), ld, P(sc), 4, layer.handle, M_TOK,
-                                      _abi.CRT_OUT_BF16, P(y), N, sp))
+        if v3:
+            _abi.check(lib.crt_quant_gemm_i8(P(codes), ld, P(sc), P(rsum[codes.data_ptr()]),
+                                             layer.handle, M_TOK, _abi.CRT_OUT_BF16, P(y), N, sp))
+        else:
+            _abi.check(lib.crt_quant_gemm(P(codes), ld, P(sc), 4, layer.handle, M_TOK,
+                                          _abi.CRT_OUT_BF16, P(y), N, sp))
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
@@ -349,7 +369,9 @@ def run_ours(args):
     bf16_burst = float(peaks.get("bf16_tflops", 1590.0))
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     int8_peak = 2.0 * bf16_burst  # tcgen05 kind::i8 runs at 2x the kind::f16 rate
-    k1_bytes = {"fc1": M_TOK * D_MODEL * 2.5 + 4 * M_TOK, "fc2": M_TOK * D_FF * 2.5 + 4 * M_TOK}
+    # bf16 in + codes out + fp32 scale (+ int32 code sum for v3) per row
+    k1_bytes = {k: M_TOK * kk * (2 + cpb) + (8 if v3 else 4) * M_TOK
+                for k, kk in (("fc1", D_MODEL), ("fc2", D_FF))}
     k1_gbs = {k: k1_bytes[k] / (statistics.mean(seg[f"k1_{k}"]) * 1e-3) / 1e9 for k in k1_bytes}
     traffic = None
     try:
@@ -444,12 +466,14 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "int4",
             "data": "synthetic (seeded gaussian bf16 activations, random-init weights)",
             "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
-                       "n0": n0, "bits": "W4A4",
+                       "n0": n0, "bits": "W4A4", "k3_path": args.path,
                        "parallelism": (f"column-parallel x{world} + NCCL all-gather" if column else
                                        f"prompt replicas x{world}" if world > 1 else "single"),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "roofline": {"bound": "tensor",
-                         "kernel": "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
+                         "kernel": ("k3_v3_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, weights "
+                                    "expanded by tcgen05.cp decompression)") if v3 else
+                                   "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
                          "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",
                          "frac": k3_tops / int8_peak, "traffic": traffic,
                          "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json); "
