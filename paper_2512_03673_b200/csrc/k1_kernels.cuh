@@ -280,6 +280,52 @@ __device__ __forceinline__ int team_code_sum(const uint8_t* crow, int64_t K, int
   return r;
 }
 
+// Row code sum for K3 v3 from the lanes' register sums `csum` (accumulated
+// as the codes were stored; a pair re-written by a near-tie redecide is
+// re-summed from its own 32 bytes).  Rows whose codes come from elsewhere
+// (slow row, partial last chunk) are summed again from memory
+// (team_code_sum).
+// Called past the end-of-row barrier; two barriers, as team_code_sum.
+__device__ __forceinline__ int team_row_sum(int csum, bool resum, const uint8_t* crow, int64_t K,
+                                            int W, int w, TeamScratch* ts, int team) {
+  const int lane = threadIdx.x & 31;
+  csum = __reduce_add_sync(0xffffffffu, csum);
+  bool any = __any_sync(0xffffffffu, resum);
+  if (W > 1) {
+    if (lane == 0) {
+      ts->i[team * W + w] = csum;
+      ts->f[team * W + w] = any ? 1.f : 0.f;
+    }
+    named_bar_sync(1 + team, W * 32);
+    csum = 0;
+    for (int i = 0; i < W; ++i) {
+      csum += ts->i[team * W + i];
+      any |= ts->f[team * W + i] != 0.f;
+    }
+    named_bar_sync(1 + team, W * 32);
+  }
+  return any ? team_code_sum(crow, K, W, w, ts, team) : csum;
+}
+
+// Code sum of the two int8-code chunks of a pair, re-read after a redecide
+// re-wrote some of their bytes (own stores, or the warp's after __syncwarp).
+template <bool FULL>
+__device__ __forceinline__ int reread_pair_sum(const uint8_t* crow, int64_t c0, int64_t cstride,
+                                               int64_t nchunks) {
+  int r = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0 + h * cstride;
+    if (!FULL && chunk >= nchunks) continue;
+    const uint4 v = *reinterpret_cast<const uint4*>(crow + chunk * 16);
+    r = __dp4a((int)v.x, 0x01010101, r);
+    r = __dp4a((int)v.y, 0x01010101, r);
+    r = __dp4a((int)v.z, 0x01010101, r);
+    r = __dp4a((int)v.w, 0x01010101, r);
+  }
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // Radix-4 butterflies on fp32x2 pairs.  H4 = J - 2*antidiag, so with
 // S = ((a+b)+c)+d:  y_j = S - 2 x_{3-j}  (form B).
@@ -560,7 +606,8 @@ __device__ __noinline__ void k1_slow_row_codes(const void* rowp, uint8_t* crow, 
 // binary, one XOR per word turns it into two's-complement nibbles.
 template <int BITS, bool FULL>
 __device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], uint8_t* crow,
-                                                 int64_t c0, int64_t cstride, int64_t nchunks) {
+                                                 int64_t c0, int64_t cstride, int64_t nchunks,
+                                                 int& csum) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t chunk = c0 + h * cstride;
@@ -581,7 +628,10 @@ __device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], ui
       for (int q = 0; q < 4; ++q) {
         wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                              __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040), 0x5410);
-        if constexpr (BITS == 5) wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+        if constexpr (BITS == 5) {
+          wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+          csum = __dp4a((int)wds[q], 0x01010101, csum);
+        }
       }
       *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
     }
@@ -806,6 +856,8 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     if (invalid && lane == 0 && w == 0) flag_invalid_value(a.err);
 
     uint8_t* crow = a.codes + row * a.ldc;
+    int csum = 0;                       // this lane's code sum (BITS == 5)
+    bool resum = (a.K & 15) != 0;       // register sums stale -> re-read the row
     if (!slow_row) {
       // ---- pass 2: certified quantisation + pack + store (see k1_fast) -------
       const float inv = amax_ref == 0.0 ? (float)rk
@@ -833,7 +885,8 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
           tb[0][i] = __float_as_uint(t.x);
           tb[1][i] = __float_as_uint(t.y);
         }
-        store_codes_pair<BITS, FULL>(tb, crow, c0, cstride, nchunks);
+        int ps = 0;  // this pair's code sum (BITS == 5)
+        store_codes_pair<BITS, FULL>(tb, crow, c0, cstride, nchunks, ps);
         uint32_t fm = 0u;
         if (!(max_nan(max_nan(em[0], em[1]), max_nan(em[2], em[3])) <= thr))
           fm = near_tie_mask(v, tb, inv, mg, thr);
@@ -844,14 +897,22 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
             for (int i = 0; i < 16; ++i) vl[i] = v[i];
             k1_redecide_lane<F32, BITS, N0>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
                                             a.kind, a.rot_cols);
+            if constexpr (BITS == 5) ps = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
           }
         } else {
-          if (__any_sync(0xffffffffu, fm != 0u))
+          if (__any_sync(0xffffffffu, fm != 0u)) {
             k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
                                    a.rot_cols);
+            if constexpr (BITS == 5) {
+              __syncwarp();
+              ps = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
+            }
+          }
         }
+        csum += ps;
       }
     } else {
+      resum = true;
       k1_slow_row_codes<F32, BITS>(rowp, crow, a.chunks, W, w, nchunks, invalid, s, a.group,
                                    a.kind, a.rot_cols);
     }
@@ -864,7 +925,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
       if (a.rowsum) {
-        const int sum = team_code_sum(crow, a.K, W, w, &ts, team);
+        const int sum = team_row_sum(csum, resum, crow, a.K, W, w, &ts, team);
         if (leader) a.rowsum[row] = sum;
       }
       if (leader) {
@@ -1049,6 +1110,8 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
     if (invalid && lane == 0 && w == 0) flag_invalid_value(a.err);
 
     uint8_t* crow = a.codes + row * a.ldc;
+    int csum = 0;                       // this lane's code sum (BITS == 5)
+    bool resum = (a.K & 15) != 0;       // register sums stale -> re-read the row
     if (!slow_row) {
       // ---- certified quantisation + pack + store ------------------------------
       // t = M + rint(y*inv) with M = 1.5*2^23 (ulp 1): the low byte of its
@@ -1085,6 +1148,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
           tb[0][i] = __float_as_uint(t.x);
           tb[1][i] = __float_as_uint(t.y);
         }
+        int ps = 0;  // this pair's code sum (BITS == 5)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t chunk = c0 + h * cstride;
@@ -1107,7 +1171,10 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
               wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                                    __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
                                    0x5410);
-              if constexpr (BITS == 5) wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+              if constexpr (BITS == 5) {
+                wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
+                ps = __dp4a((int)wds[q], 0x01010101, ps);
+              }
             }
             *reinterpret_cast<uint4*>(crow + chunk * 16) =
                 make_uint4(wds[0], wds[1], wds[2], wds[3]);
@@ -1133,14 +1200,22 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
             for (int i = 0; i < 16; ++i) vl[i] = v[p][i];
             k1_redecide_lane<F32, BITS, N0>(fm, vl, rowp, crow, c0, cstride, nchunks, s, a.group,
                                         a.kind, a.rot_cols);
+            if constexpr (BITS == 5) ps = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
           }
         } else {
-          if (__any_sync(0xffffffffu, fm != 0u))
+          if (__any_sync(0xffffffffu, fm != 0u)) {
             k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, s, a.group, a.kind,
                                    a.rot_cols);
+            if constexpr (BITS == 5) {
+              __syncwarp();
+              ps = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
+            }
+          }
         }
+        csum += ps;
       }
     } else {
+      resum = true;
       k1_slow_row_codes<F32, BITS>(rowp, crow, C, W, w, nchunks, invalid, s, a.group, a.kind,
                                    a.rot_cols);
     }
@@ -1155,7 +1230,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
       if (a.rowsum) {
-        const int sum = team_code_sum(crow, a.K, W, w, &ts, team);
+        const int sum = team_row_sum(csum, resum, crow, a.K, W, w, &ts, team);
         if (leader) a.rowsum[row] = sum;
       }
       if (leader) {

@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 600 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" >> $OUT/bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --profile > $OUT/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_v2 -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_v3 -s 2 -c 1 \
   -o $OUT/k3 python bench.py --steps 2 --warmup 3 --profile > $OUT/ncu_k3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_(fast|rolled)" -s 4 -c 2 \
   -o $OUT/k1 python bench.py --steps 2 --warmup 3 --profile > $OUT/ncu_k1.log 2>&1
