@@ -480,6 +480,7 @@ crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** ou
   if (e != cudaSuccess) {
     cudaFree(w->codes);
     cudaFree(w->s32);
+    cudaFree(w->rowsum);
     delete w;
     return cuda_fail(e, "workspace alloc");
   }
