@@ -183,14 +183,54 @@ crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_sc
  * stored ONE INT8 PER CODE (values -7..7, same codes as crt_rotate_quant)
  * plus the per-row code sums, and the GEMM that consumes them.  Device
  * buffers; codes M x ld_codes (>= K) bytes, code_sums M int32.
- * crt_quant_gemm_i8 needs K % 32 == 0 and 16-byte aligned rows, else
- * UNSUPPORTED (use crt_rotate_quant + crt_quant_gemm). */
+ * crt_quant_gemm_i8 needs 16-byte aligned rows and a layer with 4-bit
+ * weights, else UNSUPPORTED (use crt_rotate_quant + crt_quant_gemm). */
 crt_status crt_rotate_quant_i8(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                                const crt_rotation_spec* rot, uint8_t* codes, int64_t ld_codes,
                                float* scales_f32, int32_t* code_sums, void* stream);
 crt_status crt_quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                              const int32_t* code_sums, const crt_layer* layer, int64_t M,
                              int32_t out_kind, void* y, int64_t ldy, void* stream);
+
+/* -------------------------------------------------------------------------
+ * Row-parallel (K-sharded) layers -- SURVEY.md 8(e) "K (row-parallel)" and
+ * 8(f) row f3 (fc1 column-parallel -> fc2 row-parallel, int32 all-reduce).
+ * Rank r of P holds input columns [r*K/P, (r+1)*K/P):
+ *   1. crt_rotated_row_absmax on its column shard of X; MAX all-reduce
+ *      (exact) -> the global per-row max |y_ref|;
+ *   2. crt_rotate_quant_amax with that max: scales and codes equal the
+ *      unsharded compute_scales / quantize (quant.cpp:10-52) on its columns;
+ *   3. crt_quant_gemm(_i8) with out_kind I32_ACC on a crt_layer_prepare_kshard
+ *      layer: partial int_gemm accumulators; SUM all-reduce (int32, exact,
+ *      order-free; the caller checks int_gemm's capacity for the full K);
+ *   4. crt_dequant: the dequant loop of forward (pipeline.cpp:224-230).
+ * The result equals the unsharded forward bit for bit. */
+
+/* K-shard of a layer: the full layer is prepared (per-channel scales over all
+ * of K, pipeline.cpp:158-176) and input columns [rank*K/nranks,
+ * (rank+1)*K/nranks) of its codes are kept.  SHAPE if K % nranks != 0, if a
+ * rotation group would straddle shards (global rotation, K/nranks % n0 != 0)
+ * or if an odd 4-bit shard would split a packed byte. */
+crt_status crt_layer_prepare_kshard(const crt_layer_desc* desc, const void* w, int64_t ldw,
+                                    const float* bias, int32_t rank, int32_t nranks,
+                                    void* stream, crt_layer** out);
+
+/* K1 with given exact per-row maxima amax_rows (device, M doubles; +inf ->
+ * InvalidValueError at the next crt_device_status, like compute_scales).
+ * row_sums != NULL (bits 4 only): codes one int8 per code + per-row code
+ * sums (crt_quant_gemm_i8 operand); else the crt_rotate_quant layout. */
+crt_status crt_rotate_quant_amax(const void* x, int32_t x_dtype, int64_t M, int64_t K,
+                                 int64_t ldx, const crt_rotation_spec* rot,
+                                 const double* amax_rows, int32_t bits, uint8_t* codes,
+                                 int64_t ld_codes, float* scales_f32, double* scales_f64,
+                                 int32_t* row_sums, void* stream);
+
+/* Dequant of int32 accumulators (M x N, ld_acc elements) summed outside K3:
+ * y = acc * s_a[m] * s_w[n] + b[n] with the K3 epilogue's fp32 expression
+ * (forward, pipeline.cpp:224-230), bf16 / f32 / int32 copy per out_kind. */
+crt_status crt_dequant(const int32_t* acc, int64_t ld_acc, int64_t M, const float* a_scales,
+                       const crt_layer* layer, int32_t out_kind, void* y, int64_t ldy,
+                       void* stream);
 
 /* -------------------------------------------------------------------------
  * a9: forward -- replaces pipeline.cpp:206-233: K1 on x, then K3 against the

@@ -10,15 +10,17 @@ from ._abi import (CapacityError, CudaError, Error, FormatError, InvalidOrderErr
                    InvalidValueError, ShapeError, UnsupportedError, load)
 from .tensorio import load_prepared_layer, read_tensor  # noqa: F401
 from .api import (PreparedLayer, QuantSpec, RotationKind, RotationSpec, Workspace,  # noqa: F401
-                  forward, int_gemm, launch_count, packed_row_bytes, prepare_layer,
-                  prepare_layer_shard, quant_gemm, quant_gemm_i8, regular, rotate_quantize,
-                  rotate_quantize_i8,
+                  dequant, forward, int_gemm, launch_count, packed_row_bytes, prepare_layer,
+                  prepare_layer_kshard, prepare_layer_shard, quant_gemm, quant_gemm_i8, regular,
+                  rotate_quantize, rotate_quantize_amax, rotate_quantize_i8,
                   rotate_quantize_into, sylvester)
 
 __all__ = [
     "Error", "InvalidOrderError", "InvalidValueError", "ShapeError", "CapacityError",
     "FormatError", "CudaError", "UnsupportedError", "RotationKind", "RotationSpec", "QuantSpec",
-    "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "rotate_quantize_into", "prepare_layer",
-    "prepare_layer_shard", "forward", "quant_gemm", "quant_gemm_i8", "rotate_quantize_i8", "int_gemm", "launch_count",
+    "PreparedLayer", "Workspace", "regular", "sylvester", "rotate_quantize", "rotate_quantize_into",
+    "prepare_layer", "prepare_layer_shard", "prepare_layer_kshard", "forward", "quant_gemm",
+    "quant_gemm_i8", "rotate_quantize_i8", "rotate_quantize_amax", "dequant", "int_gemm",
+    "launch_count",
     "packed_row_bytes", "load", "load_prepared_layer", "read_tensor",
 ]

@@ -103,6 +103,11 @@ _SIGS = {
                                    _I64, _P, _P, _P]),
     "crt_quant_gemm_i8": (_I32, [_P, _I64, _P, _P, _P, _I64, _I32, _P, _I64, _P]),
     "crt_quant_gemm": (_I32, [_P, _I64, _P, _I32, _P, _I64, _I32, _P, _I64, _P]),
+    "crt_layer_prepare_kshard": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _I32, _I32, _P,
+                                        ctypes.POINTER(_P)]),
+    "crt_rotate_quant_amax": (_I32, [_P, _I32, _I64, _I64, _I64, ctypes.POINTER(RotationSpecC),
+                                     _P, _I32, _P, _I64, _P, _P, _P, _P]),
+    "crt_dequant": (_I32, [_P, _I64, _I64, _P, _P, _I32, _P, _I64, _P]),
     "crt_workspace_create": (_I32, [_I64, _I64, ctypes.POINTER(_P)]),
     "crt_workspace_destroy": (_I32, [_P]),
     "crt_forward": (_I32, [_P, _P, _I32, _I64, _I64, _I32, _I32, _P, _I64, _P, _P]),

@@ -196,7 +196,7 @@ class PreparedLayer:
             pass
 
 
-def _prepare(w, bias, rotation, wq, name, rank, nranks):
+def _prepare(w, bias, rotation, wq, name, rank, nranks, kshard=False):
     _check_2d_cuda(w, "w")
     if not w.is_contiguous() and w.stride(1) != 1:
         raise ShapeError("w must be row-major")
@@ -209,13 +209,19 @@ def _prepare(w, bias, rotation, wq, name, rank, nranks):
     h = ctypes.c_void_p()
     with torch.cuda.device(w.device):
         st = _stream(w)
-        if nranks == 1:
+        if kshard:
+            check(_lib().crt_layer_prepare_kshard(ctypes.byref(desc), _ptr(w), w.stride(0),
+                                                  _ptr(bias), rank, nranks, st, ctypes.byref(h)))
+        elif nranks == 1:
             check(_lib().crt_layer_prepare(ctypes.byref(desc), _ptr(w), w.stride(0), _ptr(bias),
                                            st, ctypes.byref(h)))
         else:
             check(_lib().crt_layer_prepare_shard(ctypes.byref(desc), _ptr(w), w.stride(0),
                                                  _ptr(bias), rank, nranks, st, ctypes.byref(h)))
         check(_lib().crt_device_status(st, 1))
+    if kshard:
+        return PreparedLayer(h.value, N, K // nranks, rotation, wq, bias is not None, name,
+                             w.device, (rank, nranks))
     return PreparedLayer(h.value, N // nranks, K, rotation, wq, bias is not None, name, w.device,
                          (rank, nranks))
 
@@ -229,6 +235,13 @@ def prepare_layer_shard(w: torch.Tensor, bias: Optional[torch.Tensor], rotation:
                         wq: QuantSpec, rank: int, nranks: int, name: str = "") -> PreparedLayer:
     """Column-parallel shard: output channels [rank*N/P, (rank+1)*N/P)."""
     return _prepare(w, bias, rotation, wq, name, rank, nranks)
+
+
+def prepare_layer_kshard(w: torch.Tensor, bias: Optional[torch.Tensor], rotation: RotationSpec,
+                         wq: QuantSpec, rank: int, nranks: int, name: str = "") -> PreparedLayer:
+    """Row-parallel shard: input columns [rank*K/P, (rank+1)*K/P) of the full
+    layer's codes, with the full layer's per-channel scales and bias."""
+    return _prepare(w, bias, rotation, wq, name, rank, nranks, kshard=True)
 
 
 # ---------------------------------------------------------------------------
@@ -325,6 +338,43 @@ def rotate_quantize_i8(x: torch.Tensor, rotation: RotationSpec):
     check(_lib().crt_rotate_quant_i8(_ptr(x), _dtype_code(x), M, K, x.stride(0), ctypes.byref(rc),
                                      _ptr(codes), ld, _ptr(s32), _ptr(sums), _stream(x)))
     return codes, s32, sums
+
+
+def rotate_quantize_amax(x: torch.Tensor, rotation: RotationSpec, amax: torch.Tensor,
+                         int8_codes: bool = True, bits: int = 4):
+    """K1 on a column shard with the GLOBAL exact per-row maxima ``amax``
+    (float64, device): returns (codes, fp32 scales, code sums or None).
+    int8_codes: the crt_quant_gemm_i8 layout (bits 4 only); else packed."""
+    _check_2d_cuda(x, "x")
+    M, K = x.shape
+    if amax.dtype != torch.float64 or amax.numel() != M or not amax.is_contiguous():
+        raise ShapeError("amax must be a contiguous float64 vector of M rows")
+    if int8_codes and bits != 4:
+        raise InvalidValueError("int8-stored codes are for 4-bit activations")
+    row = K if (int8_codes or bits == 8) else (K + 1) // 2
+    ld = max(16, (row + 15) // 16 * 16)
+    codes = torch.empty((M, ld), dtype=torch.uint8, device=x.device)
+    s32 = torch.empty(M, dtype=torch.float32, device=x.device)
+    sums = torch.empty(M, dtype=torch.int32, device=x.device) if int8_codes else None
+    rc = rotation.c()
+    check(_lib().crt_rotate_quant_amax(_ptr(x), _dtype_code(x), M, K, x.stride(0), ctypes.byref(rc),
+                                       _ptr(amax), bits, _ptr(codes), ld, _ptr(s32), None,
+                                       _ptr(sums), _stream(x)))
+    return codes, s32, sums
+
+
+def dequant(acc: torch.Tensor, scales: torch.Tensor, layer: PreparedLayer, *, out: str = "bf16",
+            y: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The dequant loop of forward (pipeline.cpp:224-230) on int32
+    accumulators summed outside K3 (row-parallel all-reduce)."""
+    if acc.dtype != torch.int32 or acc.dim() != 2 or acc.stride(1) != 1:
+        raise ShapeError("acc must be a row-major int32 matrix")
+    M = acc.shape[0]
+    if y is None:
+        y = torch.empty((M, layer.out_features), dtype=_OUT_DTYPE[out], device=acc.device)
+    check(_lib().crt_dequant(_ptr(acc), acc.stride(0), M, _ptr(scales), layer.handle, _OUT[out],
+                             _ptr(y), y.stride(0), _stream(acc)))
+    return y
 
 
 def quant_gemm_i8(codes: torch.Tensor, scales: torch.Tensor, sums: torch.Tensor,

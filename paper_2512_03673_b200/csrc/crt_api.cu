@@ -1,9 +1,11 @@
 // crt_api.cu -- the C-ABI (include/crt/convlinear4bit.h): host-side
 // validation with the reference's error behaviour, resource ownership, and
 // the launches of K1 (rotate+quant), K2 (weight prep) and K3 (GEMM).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cmath>
@@ -88,7 +90,7 @@ crt_status resolve_rotation(const crt_rotation_spec* rot, int64_t cols, int64_t*
 crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                   const crt_rotation_spec* rot, int32_t bits, uint8_t* codes, int64_t ldc,
                   float* s32, double* s64, cudaStream_t st, double* amax = nullptr,
-                  int32_t* rowsum = nullptr) {
+                  int32_t* rowsum = nullptr, const double* amax_in = nullptr) {
   // bits 5 (internal): 4-bit codes stored one int8 per code, + row code sums
   if (x_dtype != CRT_DTYPE_BF16 && x_dtype != CRT_DTYPE_F32)
     return fail(CRT_ERR_INVALID_VALUE, "unsupported input dtype");
@@ -126,6 +128,7 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
   a.s64 = s64;
   a.amax = amax;
   a.rowsum = rowsum;
+  a.amax_in = amax_in;
   a.err = device_error_word();
   if (!a.err) return fail(CRT_ERR_CUDA, "device error word allocation failed");
   crt::K1Plan plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx,
@@ -201,6 +204,24 @@ crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K
   if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
   return run_k1(x, x_dtype, M, K, ldx, rot, bits, codes, ld_codes, scales_f32, scales_f64,
                 (cudaStream_t)stream);
+}
+
+// Row-parallel K1: quantise a column shard of X with the GLOBAL exact row
+// maxima `amax_rows` (the MAX all-reduce of every shard's
+// crt_rotated_row_absmax), so scales and codes equal the unsharded
+// compute_scales / quantize (quant.cpp:10-52) on those columns.
+// row_sums != null (bits 4 only) stores the codes one int8 per code with the
+// per-row code sums (crt_quant_gemm_i8 operand); else packed / int8 by bits.
+crt_status crt_rotate_quant_amax(const void* x, int32_t x_dtype, int64_t M, int64_t K,
+                                 int64_t ldx, const crt_rotation_spec* rot,
+                                 const double* amax_rows, int32_t bits, uint8_t* codes,
+                                 int64_t ld_codes, float* scales_f32, double* scales_f64,
+                                 int32_t* row_sums, void* stream) {
+  if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
+  if (!amax_rows && M > 0) return fail(CRT_ERR_INVALID_VALUE, "null amax_rows");
+  if (row_sums && bits != 4) return fail(CRT_ERR_INVALID_VALUE, "row sums are for 4-bit codes");
+  return run_k1(x, x_dtype, M, K, ldx, rot, row_sums ? 5 : bits, codes, ld_codes, scales_f32,
+                scales_f64, (cudaStream_t)stream, nullptr, row_sums, amax_rows);
 }
 
 // f4: outlier_amplitude(group_rotate(x)) per row (analysis.cpp:12-17,
@@ -364,6 +385,71 @@ crt_status crt_layer_prepare_shard(const crt_layer_desc* desc, const void* w, in
   return prepare_impl(desc, w, ldw, bias, rank, nranks, (cudaStream_t)stream, out);
 }
 
+// Row-parallel (K-sharded) layer: rank r keeps
+// input columns [r*K/P, (r+1)*K/P) of the full layer's codes.  The
+// per-channel scales are the full layer's (prepare_layer quantises each
+// output channel over all of K, pipeline.cpp:158-176), so the shards' int32
+// partial accumulators sum to int_gemm's exactly.  Rotation groups must not
+// straddle shards.
+crt_status crt_layer_prepare_kshard(const crt_layer_desc* d, const void* w, int64_t ldw,
+                                    const float* bias, int32_t rank, int32_t nranks,
+                                    void* stream, crt_layer** out) {
+  if (!d || !out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(CRT_ERR_INVALID_VALUE, "bad rank / nranks");
+  const int64_t N = d->out_features, K = d->in_features;
+  if (K < 0 || N < 0) return fail(CRT_ERR_SHAPE, "negative shape");
+  if (K % nranks != 0) return fail(CRT_ERR_SHAPE, "in_features not divisible by nranks");
+  const int64_t Ks = K / nranks;
+  int64_t group = 1, rot_cols = K;
+  crt_status rs = resolve_rotation(&d->rotation, K, &group, &rot_cols);
+  if (rs != CRT_OK) return rs;
+  if (rot_cols != K || (group > 1 && Ks % group != 0) ||
+      (d->rotation.kind != CRT_ROT_NONE && d->rotation.group_size == 0 && nranks > 1))
+    return fail(CRT_ERR_SHAPE, "rotation groups would straddle the K shards");
+  if (d->bits_w == 4 && Ks % 2 != 0) return fail(CRT_ERR_SHAPE, "odd K shard splits a packed byte");
+  cudaStream_t st = (cudaStream_t)stream;
+  crt_layer* full = nullptr;
+  crt_status s = prepare_impl(d, w, ldw, bias, 0, 1, st, &full);
+  if (s != CRT_OK) return s;
+  crt_layer* L = new crt_layer();
+  L->desc = *d;
+  L->desc.in_features = Ks;
+  L->n_total = N;
+  L->row_offset = 0;
+  const int64_t row = d->bits_w == 4 ? Ks / 2 : Ks;
+  L->ldc = (row + 15) / 16 * 16;
+  const size_t nalloc = (size_t)(N ? N : 1);
+  cudaError_t e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
+  if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
+  if (e == cudaSuccess && bias) e = cudaMalloc(&L->bias, 4 * nalloc);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L->codes, 0, (size_t)L->ldc * nalloc, st);
+  if (e == cudaSuccess && N && row)
+    e = cudaMemcpy2DAsync(L->codes, L->ldc, full->codes + (int64_t)rank * row, full->ldc, row, N,
+                          cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s32, full->s32, 4 * N, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s64, full->s64, 8 * N, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && bias && N)
+    e = cudaMemcpyAsync(L->bias, full->bias, 4 * N, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  crt_layer_destroy(full);
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "kshard copy");
+  }
+  int64_t launches = 0;
+  e = crt::k3_prepare_weights(L->codes, L->ldc, N, Ks, d->bits_w, &L->tiles, st, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess) {
+    crt_layer_destroy(L);
+    return cuda_fail(e, "weight tiling");
+  }
+  *out = L;
+  return CRT_OK;
+}
+
 crt_status crt_layer_destroy(crt_layer* L) {
   if (!L) return CRT_OK;
   cudaFree(L->codes);
@@ -465,6 +551,49 @@ crt_status crt_quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a
                              int32_t out_kind, void* y, int64_t ldy, void* stream) {
   if (!code_sums) return fail(CRT_ERR_INVALID_VALUE, "null code_sums");
   return quant_gemm_impl(a_codes, lda, a_scales, code_sums, 1, 4, L, M, out_kind, y, ldy, stream);
+}
+
+// The dequant loop of forward (pipeline.cpp:224-230) on int32 accumulators
+// that were summed outside K3 (row-parallel: the SUM all-reduce of the
+// shards' partial int_gemm results).  Same fp32 expression as the K3
+// epilogues, so the output equals the unsharded forward bit for bit.
+__global__ void crt_dequant_kernel(const int32_t* __restrict__ acc, int64_t lda, int64_t M,
+                                   int64_t N, const float* __restrict__ sa,
+                                   const float* __restrict__ sw, const float* __restrict__ bias,
+                                   int32_t out_kind, void* y, int64_t ldy) {
+  const int64_t total = M * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / N, n = i - m * N;
+    const int32_t v = acc[m * lda + n];
+    if (out_kind == CRT_OUT_I32_ACC) {
+      reinterpret_cast<int32_t*>(y)[m * ldy + n] = v;
+      continue;
+    }
+    const float r = fmaf((float)v * sa[m], sw[n], bias ? bias[n] : 0.f);
+    if (out_kind == CRT_OUT_BF16) reinterpret_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(r);
+    else reinterpret_cast<float*>(y)[m * ldy + n] = r;
+  }
+}
+
+crt_status crt_dequant(const int32_t* acc, int64_t ld_acc, int64_t M, const float* a_scales,
+                       const crt_layer* L, int32_t out_kind, void* y, int64_t ldy, void* stream) {
+  if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
+  if (out_kind < CRT_OUT_BF16 || out_kind > CRT_OUT_I32_ACC)
+    return fail(CRT_ERR_INVALID_VALUE, "bad out_kind");
+  const int64_t N = L->desc.out_features;
+  if (M < 0) return fail(CRT_ERR_SHAPE, "negative M");
+  if (M == 0 || N == 0) return CRT_OK;
+  if (ld_acc < N || ldy < N) return fail(CRT_ERR_SHAPE, "ld < N");
+  if (!acc || !y || !a_scales) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
+  const int64_t total = M * N;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  crt_dequant_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      acc, ld_acc, M, N, a_scales, L->s32, L->bias, out_kind, y, ldy);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "dequant launch");
+  return CRT_OK;
 }
 
 crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** out) {

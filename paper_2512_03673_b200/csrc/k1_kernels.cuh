@@ -851,6 +851,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
                                                   a.kind, a.rot_cols),
                             &ts, team, w, W);
     }
+    if (a.amax_in) amax_ref = a.amax_in[row];  // global row max (row-parallel shard)
     const bool invalid = !isfinite(amax_ref);
     const double s = invalid ? 1.0 : (amax_ref == 0.0 ? 1.0 : amax_ref / (double)QMAX);
     if (invalid && lane == 0 && w == 0) flag_invalid_value(a.err);
@@ -952,9 +953,12 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
 // ---------------------------------------------------------------------------
 constexpr int kK1FThreads = 192;  // 6 warps; two CTAs per SM at <= 170 registers
 constexpr int kK1FMinBlocks = 2;
+// CTAs per SM the single-pass kernel is compiled for: fewer register-resident
+// chunks per lane leave room for more warps (C <= 2: 85 registers, 4 CTAs).
+constexpr int k1_fast_min_blocks(int C) { return C <= 2 ? 4 : (C <= 4 ? 3 : kK1FMinBlocks); }
 
 template <int C, int N0, bool F32, int BITS, bool BULK, bool FULL>
-__global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) {
+__global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1Args a) {
   constexpr int P = C / 2;
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
@@ -1105,6 +1109,7 @@ __global__ void __launch_bounds__(kK1FThreads, kK1FMinBlocks) k1_fast(K1Args a) 
                                                   a.rot_cols),
                             &ts, team, w, W);
     }
+    if (a.amax_in) amax_ref = a.amax_in[row];  // global row max (row-parallel shard)
     const bool invalid = !isfinite(amax_ref);
     const double s = invalid ? 1.0 : (amax_ref == 0.0 ? 1.0 : amax_ref / (double)QMAX);
     if (invalid && lane == 0 && w == 0) flag_invalid_value(a.err);
@@ -1284,6 +1289,10 @@ __global__ void __launch_bounds__(256) k1_exact(K1Args a) {
       bad |= redbad[i];
     }
     __syncthreads();
+    if (a.amax_in) {  // global row max (row-parallel shard)
+      m = a.amax_in[row];
+      bad = !isfinite(m);
+    }
     double s = bad ? 1.0 : (m == 0.0 ? 1.0 : m / (double)QMAX);
     if (bad && tid == 0) flag_invalid_value(a.err);
     for (int64_t j = tid; j < a.K; j += blockDim.x) {
@@ -1391,7 +1400,7 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   teams = teams < 1 ? 1 : (teams > kK1MaxTeams ? kK1MaxTeams : teams);
   const int64_t rows_per_sm = (a.M + num_sms - 1) / num_sms;
   if (teams > rows_per_sm) teams = (int)(rows_per_sm < 1 ? 1 : rows_per_sm);
-  const size_t budget = (size_t)216 * 1024 / kK1FMinBlocks;
+  const size_t budget = (size_t)216 * 1024 / k1_fast_min_blocks(C);
   int S = (int)(budget / ((size_t)teams * rb));
   if (S > kK1MaxStages) S = kK1MaxStages;
   const bool bulk = S >= 1 && ((uintptr_t)a.x % 16 == 0) && ((a.ldx * (F32 ? 4 : 2)) % 16 == 0);
@@ -1442,7 +1451,9 @@ cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
       if (e != cudaErrorInvalidValue) return e;
     }
   }
-  if (a.team_warps > 1) return launch_rolled<N0, F32, BITS>(a, st, l);
+  static const bool fast_teams = getenv("CRT_K1_FAST_TEAMS") != nullptr;  // dev aid (sweeps)
+  if (a.team_warps > 1 && !(fast_teams && a.chunks <= 8))
+    return launch_rolled<N0, F32, BITS>(a, st, l);
   switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
     case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
     case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);

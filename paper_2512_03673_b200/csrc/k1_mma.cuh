@@ -433,7 +433,7 @@ inline bool mma_path_ok(const K1Args& a, int n0, bool f32) {
     const char* e = getenv("CRT_K1_MMA");
     return e && e[0] == '1';
   }();
-  if (!on || f32 || a.kind != kRotRegular || (n0 != 4 && n0 != 16)) return false;
+  if (!on || f32 || a.amax_in || a.kind != kRotRegular || (n0 != 4 && n0 != 16)) return false;
   if (a.K % 256 != 0 || a.rot_cols != a.K) return false;
   if ((uintptr_t)a.x % 16 || (a.ldx * 2) % 16 || (uintptr_t)a.codes % 16 || a.ldc % 16) return false;
   return (size_t)a.K * 2 <= (size_t)216 * 1024 / kK1MMinBlocks;

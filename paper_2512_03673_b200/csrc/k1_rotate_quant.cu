@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "k1_rotate_quant.h"
+#include <stdio.h>
 
 namespace crt {
 
@@ -51,7 +52,18 @@ K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, in
       if (C <= 8) C = 10;
     }
   }
-  const int bestC = (int)C, bestW = (int)W;
+  int bestC = (int)C, bestW = (int)W;
+  // dev aid: CRT_K1_PLAN="W,C" forces the team shape (single-pass when W <= 6,
+  // C <= 8 and C even) -- used by tools/k1_sweep.sh
+  static const char* force = getenv("CRT_K1_PLAN");
+  if (force) {
+    int fw = 0, fc = 0;
+    if (sscanf(force, "%d,%d", &fw, &fc) == 2 && fw >= 1 && fw <= 8 && fc >= 2 && fc % 2 == 0 &&
+        (int64_t)fw * 32 * fc >= nchunks) {
+      bestW = fw;
+      bestC = fc;
+    }
+  }
   p.fast = true;
   p.C = bestC;
   p.W = bestW;

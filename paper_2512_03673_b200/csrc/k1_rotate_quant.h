@@ -23,6 +23,8 @@ struct K1Args {
   double* s64;        // nullable
   double* amax;       // nullable: exact per-row max |y_ref| (outlier_amplitude)
   int32_t* rowsum;    // nullable: per-row sum of the int8 codes (bits 5 layout)
+  const double* amax_in;  // nullable: use this exact per-row max |y_ref| for the scale
+                          // (row-parallel: the MAX all-reduce of the shards' maxima)
   int* err;           // device error word
 };
 

@@ -10,6 +10,15 @@ plumbing.  Two strategies, both bit-identical to one GPU:
   scales span the full K exactly like the reference), then K3 on its shard.
   The shards are reassembled with one ``all_gather_into_tensor`` (rank-major
   [P][M][N/P]) and a column interleave into [M, N].
+* Row parallel (SURVEY.md 8e "K", 8f row f3; e.g. FLUX fc2 K = 12288, fed by
+  the column-parallel fc1 whose output shard IS this rank's input shard):
+  rank r owns input columns [r*K/P, (r+1)*K/P) of the full layer's codes
+  (``crt_layer_prepare_kshard``: per-channel scales over all of K).  Each
+  rank computes the exact max |group_rotate(x)| of its columns, one MAX
+  all-reduce (M doubles) gives the global per-token max, so K1 produces
+  exactly the unsharded scales and codes on its columns; K3 yields int32
+  partial accumulators and one SUM all-reduce (int32: exact, order-free)
+  gives int_gemm's result, dequantised once (``crt_dequant``).
 * Prompt (batch) sharding: independent prompts go to ranks round-robin; no
   collective on the data path.
 
@@ -83,14 +92,88 @@ class ColumnParallelLinear:
         obj.layer = layer
         return obj
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, gather: bool = True) -> torch.Tensor:
+        """gather=False returns this rank's [M, N/P] shard -- the input shard
+        of a following RowParallelLinear (no collective between them)."""
         shard = self.local_forward(x).contiguous()
-        if self.nranks == 1:
+        if self.nranks == 1 or not gather:
             return shard
         gathered = torch.empty((self.nranks * shard.shape[0], shard.shape[1]), dtype=shard.dtype,
                                device=shard.device)
         dist.all_gather_into_tensor(gathered, shard, group=self.group)
         return interleave_rank_major(gathered, self.nranks)
+
+    __call__ = forward
+
+
+INT32_MAX = 2147483647
+
+
+class RowParallelLinear:
+    """A ConvLinear4bit layer sharded over input features.
+
+    ``forward(x_shard)`` takes this rank's [M, K/P] input columns and returns
+    the full [M, N] output on every rank, equal to the unsharded forward bit
+    for bit.  The local steps are injectable (CPU tests use the oracle):
+      local_amax(x_shard) -> float64 [M]: exact max |group_rotate| of the shard
+      local_partial(x_shard, amax) -> (int32 [M, N] partial acc, fp32/f64 [M] scales)
+      dequant(acc, scales) -> y
+    """
+
+    def __init__(self, in_features: int, out_features: int, local_amax, local_partial, dequant,
+                 bits: Tuple[int, int] = (4, 4), group: Optional[dist.ProcessGroup] = None):
+        self.group = group
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.in_features, self.out_features = in_features, out_features
+        self.cols = shard_range(in_features, self.rank, self.nranks)
+        qa, qw = (1 << (bits[0] - 1)) - 1, (1 << (bits[1] - 1)) - 1
+        if qa * qw * in_features > INT32_MAX:  # int_gemm capacity, pipeline.cpp:184-192
+            from ._abi import CapacityError
+            raise CapacityError(f"int_gemm: {in_features}-deep accumulation can overflow int32")
+        self.local_amax, self.local_partial, self.dequant = local_amax, local_partial, dequant
+
+    @classmethod
+    def from_weights(cls, w: torch.Tensor, bias: Optional[torch.Tensor], rotation, wq, aq,
+                     out: str = "bf16", group: Optional[dist.ProcessGroup] = None,
+                     name: str = ""):
+        """CUDA path: this rank's K-shard prepared with the sm_100a kernels."""
+        from . import api
+        from .analysis import rotated_row_absmax
+        nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        layer = api.prepare_layer_kshard(w, bias, rotation, wq, rank, nranks, name)
+        i8 = aq.bits == 4 and wq.bits == 4
+
+        def local_amax(xs):
+            return rotated_row_absmax(xs, rotation)
+
+        def local_partial(xs, amax):
+            codes, s32, sums = api.rotate_quantize_amax(xs, rotation, amax, int8_codes=i8,
+                                                        bits=aq.bits)
+            if i8:
+                acc = api.quant_gemm_i8(codes, s32, sums, layer, out="i32")
+            else:
+                acc = api.quant_gemm(codes, s32, layer, aq, out="i32")
+            return acc, s32
+
+        def deq(acc, s32):
+            return api.dequant(acc, s32, layer, out=out)
+
+        obj = cls(w.shape[1], w.shape[0], local_amax, local_partial, deq, (aq.bits, wq.bits),
+                  group)
+        obj.layer = layer
+        return obj
+
+    def forward(self, x_shard: torch.Tensor) -> torch.Tensor:
+        amax = self.local_amax(x_shard).contiguous()
+        if self.nranks > 1:
+            dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=self.group)
+        acc, scales = self.local_partial(x_shard, amax)
+        acc = acc.contiguous()
+        if self.nranks > 1:
+            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
+        return self.dequant(acc, scales)
 
     __call__ = forward
 
