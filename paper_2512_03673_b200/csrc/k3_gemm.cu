@@ -389,6 +389,7 @@ cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
     if (k3_v3_supported(a)) return k3_v3_launch(a, st, launches);
     return cudaErrorInvalidValue;
   }
+  if (!force_v1 && a.bits == 8 && k3_v3_supported(a)) return k3_v3_launch(a, st, launches);
   if (!force_v1 && k3_v2_supported(a)) return k3_v2_launch(a, st, launches);
   const bool b4 = a.bits == 4;
   const bool aligned = ((uintptr_t)a.a_codes % 16 == 0) && (a.lda % 16 == 0) &&

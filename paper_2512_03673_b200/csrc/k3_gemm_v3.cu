@@ -48,6 +48,7 @@ constexpr int V3_STAGE = V3_A_STAGE + V3_B_STAGE;
 // data bytes (64 per row), not its padded smem footprint (128 per row) --
 // measured, tools/probes/tma_u4_probe.cu
 constexpr int V3_STAGE_TX = V3_BM * 64 + V3_B_STAGE;
+constexpr int V3_STAGE_TX_W8 = V3_BM * 128 + V3_B_STAGE;  // W8A8: int8 weights, no padding
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the pair bit: CTA 0's barrier
 
 struct V3Smem {
@@ -150,6 +151,10 @@ __device__ __forceinline__ void tc_cp_decompress(uint32_t taddr, uint64_t sdesc)
                "l"(sdesc)
                : "memory");
 }
+// W8A8: int8 weights copied as they are (same 128 B/row smem layout).
+__device__ __forceinline__ void tc_cp_raw(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void tc_mma_pair_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
                                                uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -188,6 +193,9 @@ struct V3Args {
   int64_t ldy;
 };
 
+// W8 = false: W4A4 (offset-binary int4 weights, hardware expansion);
+// W8 = true: W8A8 (int8 weights and activations).
+template <bool W8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     k3_v3_kernel(const __grid_constant__ CUtensorMap map_w,
                  const __grid_constant__ CUtensorMap map_x, V3Args a) {
@@ -245,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         const int m0 = tt * V3_BT + (int)rank * V3_BTH;      // this CTA's token rows
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&ss->empty[s], ph ^ 1);
-          if (leader) mbar_arrive_expect_tx(&ss->full[s], 2 * V3_STAGE_TX);
+          if (leader) mbar_arrive_expect_tx(&ss->full[s], 2 * (W8 ? V3_STAGE_TX_W8 : V3_STAGE_TX));
           else arrive_cluster(full0 + s * 8);
           uint8_t* st = stg + s * V3_STAGE;
           tma_load_2sm(st, &map_w, kb * 128, n0, &ss->full[s]);
@@ -310,7 +318,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
           const uint32_t abase = smem_u32(stg + s * V3_STAGE);
           const uint32_t acol = tmem + a_col(slot);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) tc_cp_decompress(acol + kk * 8, sw128_desc(abase + kk * 32));
+          for (int kk = 0; kk < 4; ++kk) {
+            if constexpr (W8) tc_cp_raw(acol + kk * 8, sw128_desc(abase + kk * 32));
+            else tc_cp_decompress(acol + kk * 8, sw128_desc(abase + kk * 32));
+          }
           tc_commit_leader(&ss->dec_full[slot]);
           if (++s == V3_PS) {
             s = 0;
@@ -344,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
       for (int i = et; i < V3_BT; i += 256) {
         const int64_t m = mb + i;
         ss->sa[ab][i] = m < a.M ? a.a_scales[m] : 0.f;
-        ss->sums[ab][i] = m < a.M ? 32 * a.a_sums[m] : 0;
+        ss->sums[ab][i] = (W8 || m >= a.M) ? 0 : 32 * a.a_sums[m];
       }
       named_bar_sync(1, 256);
       wait_sleep(&ss->acc_full[ab], aph);
@@ -363,14 +374,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
           if (jn == 32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int v = ((int)acc[j] - sm[j]) >> 2;
+              const int v = W8 ? (int)acc[j] : (((int)acc[j] - sm[j]) >> 2);
               yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (j < jn) {
-                const int v = ((int)acc[j] - sm[j]) >> 2;
+                const int v = W8 ? (int)acc[j] : (((int)acc[j] - sm[j]) >> 2);
                 yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
               }
           }
@@ -379,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (j < jn) {
-              const int v = ((int)acc[j] - sm[j]) >> 2;
+              const int v = W8 ? (int)acc[j] : (((int)acc[j] - sm[j]) >> 2);
               yp[j * a.ldy] = a.out_kind == 2 ? (uint32_t)v
                                               : __float_as_uint(fmaf((float)v * sa[j], sw, bn));
             }
@@ -422,10 +433,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_v3() {
 }  // namespace
 
 bool k3_v3_supported(const K3Args& a) {
-  if (a.bits != 4 || a.a_layout != 1 || !a.a_sums || !a.w.codes_ob) return false;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.K > 1277000) return false;
-  if ((uintptr_t)a.a_codes % 16 || a.lda % 16 || (uintptr_t)a.w.codes_ob % 16 || a.w.ld_ob % 64)
-    return false;
+  if ((uintptr_t)a.a_codes % 16 || a.lda % 16) return false;
+  if (a.bits == 8) {  // W8A8: int8 rows on both sides (the reference layout)
+    if (a.a_layout != 0 || !a.w.codes || (uintptr_t)a.w.codes % 16 || a.w.ld % 16) return false;
+  } else {
+    if (a.bits != 4 || a.a_layout != 1 || !a.a_sums || !a.w.codes_ob) return false;
+    if ((uintptr_t)a.w.codes_ob % 16 || a.w.ld_ob % 64) return false;
+  }
   return encode_fn_v3() != nullptr;
 }
 
@@ -438,7 +453,17 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   }
   auto fn = encode_fn_v3();
   CUtensorMap mw, mx;
-  {  // weights: N rows x K 4-bit codes (offset binary), padded 16-code units
+  const bool w8 = a.bits == 8;
+  if (w8) {  // weights: N rows x K int8 codes
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.N};
+    cuuint64_t strides[1] = {(cuuint64_t)a.w.ld};
+    cuuint32_t box[2] = {128, (cuuint32_t)V3_BM};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.w.codes), dims, strides,
+           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else {  // weights: N rows x K 4-bit codes (offset binary), padded 16-code units
     cuuint64_t dims[2] = {(cuuint64_t)(a.w.ld_ob * 2), (cuuint64_t)a.N};
     cuuint64_t strides[1] = {(cuuint64_t)a.w.ld_ob};
     cuuint32_t box[2] = {128, (cuuint32_t)V3_BM};
@@ -472,17 +497,18 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.y = a.y;
   v.ldy = a.ldy;
   const size_t smem = 1024 + V3_PS * V3_STAGE + sizeof(V3Smem);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k3_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = w8 ? k3_v3_kernel<true> : k3_v3_kernel<false>;
+  static bool attr[2] = {false, false};
+  if (!attr[w8]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[w8] = true;
   }
   const int tiles = v.ttiles * v.ctiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  k3_v3_kernel<<<(unsigned)(2 * pairs), V3_THREADS, smem, st>>>(mw, mx, v);
+  kern<<<(unsigned)(2 * pairs), V3_THREADS, smem, st>>>(mw, mx, v);
   ++*launches;
   return cudaGetLastError();
 }

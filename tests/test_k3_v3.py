@@ -67,3 +67,28 @@ def test_forward_v3_equals_packed_path(M, K, N):
     codes_p, sa = crt.rotate_quantize(x, spec)
     for out in ("i32", "f32", "bf16"):
         assert torch.equal(crt.forward(x, layer, out=out), crt.quant_gemm(codes_p, sa, layer, out=out))
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 16, 16), (7, 48, 40), (193, 160, 257), (384, 3072, 768),
+                                   (257, 3104, 1000), (1024, 12288, 512)])
+def test_v3_w8a8_accumulators_exact(M, K, N):
+    """f1: W8A8 on the v3 kernel (int8 weights copied to TMEM
+    by tcgen05.cp without decompression).  int_gemm exact; the dequantised
+    outputs equal crt_dequant of the same accumulators (one fp32 expression)."""
+    import paper_2512_03673_b200 as crt
+    from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * K + N)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    spec, q8 = RotationSpec(RotationKind.regular, 16), QuantSpec(8)
+    layer = crt.prepare_layer(w, torch.randn(N, device="cuda", generator=g), spec, q8)
+    codes, sa = crt.rotate_quantize(x, spec, q8)
+    A = codes[:, :K].view(torch.int8).to(torch.float64)
+    B = layer.export(scales64=False)[0][:, :K].view(torch.int8).to(torch.float64)
+    ref = (A @ B.T).round().to(torch.int64)
+    acc = crt.quant_gemm(codes, sa, layer, q8, out="i32")
+    assert torch.equal(acc.to(torch.int64), ref)
+    for out in ("f32", "bf16"):
+        assert torch.equal(crt.quant_gemm(codes, sa, layer, q8, out=out),
+                           crt.dequant(acc, sa, layer, out=out)), out
+    assert torch.equal(crt.forward(x, layer, q8, out="i32"), acc)
