@@ -723,7 +723,7 @@ __device__ __noinline__ double k1_cands_warp(uint32_t m, const void* rowp, int64
 constexpr int kK1MaxTeams = 8;
 constexpr int kK1MaxStages = 4;
 constexpr int kK1Threads = 256;
-constexpr int kK1MinBlocks = 3;  // rolled kernel: <= 85 registers, 24 warps per SM
+constexpr int kK1MinBlocks = 2;  // rolled kernel: <= 128 registers, 16 warps per SM
 
 template <int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) {
@@ -1442,23 +1442,29 @@ namespace crt {
 
 template <int N0, bool F32, int BITS>
 cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
-  // Multi-warp rows: the rolled kernel's occupancy (24 warps/SM) beats the
-  // register-resident one (measured: K=12288 N0=16 67.6 vs 77.8 us); one
-  // warp per row (K <= 3072): the single-pass kernel (24.6 vs 28.8 us).
+  // Default: the two-pass rolled kernel (128 registers, 16 warps/SM, no
+  // spills) -- measured faster than the register-resident single-pass kernel
+  // at every FLUX shape (M=4608: K=3072 24.6 vs 28.7 us, K=12288 69.6 vs
+  // 92.1 us; N0 sweep profiles/r01_n0_sweep.jsonl).  The single-pass kernel
+  // stays as an opt-in (CRT_K1_FAST=1, C <= 8), the tensor-core one as
+  // CRT_K1_MMA=1; tests/test_alt_paths.py keeps both bit-exact.
   if constexpr (!F32 && (N0 == 4 || N0 == 16) && BITS != 5) {
     if (mma_path_ok(a, N0, F32)) {
       const cudaError_t e = launch_mma<N0, BITS>(a, st, l);
       if (e != cudaErrorInvalidValue) return e;
     }
   }
-  static const bool fast_teams = getenv("CRT_K1_FAST_TEAMS") != nullptr;  // dev aid (sweeps)
-  if (a.team_warps > 1 && !(fast_teams && a.chunks <= 8))
-    return launch_rolled<N0, F32, BITS>(a, st, l);
-  switch (a.chunks) {  // single-pass kernels for C <= 8, rolled beyond
-    case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
-    case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);
-    case 6: return launch_fast<6, N0, F32, BITS>(a, st, l);
-    case 8: return launch_fast<8, N0, F32, BITS>(a, st, l);
+  static const bool fast = [] {
+    const char* e = getenv("CRT_K1_FAST");
+    return e && e[0] == '1';
+  }();
+  if (fast && a.team_warps == 1) {
+    switch (a.chunks) {
+      case 2: return launch_fast<2, N0, F32, BITS>(a, st, l);
+      case 4: return launch_fast<4, N0, F32, BITS>(a, st, l);
+      case 6: return launch_fast<6, N0, F32, BITS>(a, st, l);
+      case 8: return launch_fast<8, N0, F32, BITS>(a, st, l);
+    }
   }
   return launch_rolled<N0, F32, BITS>(a, st, l);
 }
