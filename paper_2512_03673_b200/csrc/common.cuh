@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace crt {
 
@@ -128,6 +129,43 @@ __device__ __forceinline__ bool regular_negative(uint32_t k, uint32_t j) {
 // Sylvester (hadamard.cpp:70-89): H[k][j] = (-1)^popcount(k & j).
 __device__ __forceinline__ bool sylvester_negative(uint32_t k, uint32_t j) {
   return (__popc(k & j) & 1u) != 0;
+}
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  A kernel launched with
+// launch_pdl may start (prologue: barriers, TMEM, descriptor prefetch) while
+// its stream predecessor drains; every thread calls griddep_wait() before
+// its first global-memory access (read OR write: forward reuses the
+// workspace, so the next K1 must not overwrite codes the previous K3 still
+// reads).  griddep_launch() lets this kernel's own successor be scheduled.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CRT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 }  // namespace crt

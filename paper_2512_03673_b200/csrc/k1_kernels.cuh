@@ -221,10 +221,14 @@ struct TeamScratch {
   float f[32];
   double d[32];
   int i[32];
+  int rs[8][2];  // per team, per row parity: code sum of the row (rowsum_publish)
+  int rf[8][2];  // per team, per row parity: "re-sum from memory" flag
 };
 
-// Team of W warps (contiguous warps team*W .. team*W+W-1).  Two barriers
-// make the slot reusable immediately.
+// Team of W warps (contiguous warps team*W .. team*W+W-1).  ONE barrier per
+// reduction: each reduction owns its slot array (f, d), and a slot is written
+// again only in the next row, after a later team barrier that every warp
+// reaches only once it has read the slot.
 __device__ __forceinline__ float team_max_nan(float v, TeamScratch* ts, int team, int w,
                                               int W) {
   v = warp_max_nan(v);
@@ -234,7 +238,6 @@ __device__ __forceinline__ float team_max_nan(float v, TeamScratch* ts, int team
   named_bar_sync(1 + team, W * 32);
   float r = ts->f[team * W];
   for (int i = 1; i < W; ++i) r = max_nan(r, ts->f[team * W + i]);
-  named_bar_sync(1 + team, W * 32);
   return r;
 }
 __device__ __forceinline__ double team_max_d(double v, TeamScratch* ts, int team, int w,
@@ -246,7 +249,6 @@ __device__ __forceinline__ double team_max_d(double v, TeamScratch* ts, int team
   named_bar_sync(1 + team, W * 32);
   double r = ts->d[team * W];
   for (int i = 1; i < W; ++i) r = fmax(r, ts->d[team * W + i]);
-  named_bar_sync(1 + team, W * 32);
   return r;
 }
 
@@ -305,6 +307,31 @@ __device__ __forceinline__ int team_row_sum(int csum, bool resum, const uint8_t*
     named_bar_sync(1 + team, W * 32);
   }
   return any ? team_code_sum(crow, K, W, w, ts, team) : csum;
+}
+
+// Row code sums for teams (W > 1) without extra barriers: before the
+// end-of-row barrier each warp adds its sum (and its "re-sum" flag) into the
+// team's slot for this row's parity with shared-memory atomics; after the
+// barrier every warp reads the flag (uniform decision), the leader the sum.
+// The leader clears the slot in the NEXT row after its first team barrier
+// (rowsum_clear), when every warp has read it; the row after that reuses it.
+__device__ __forceinline__ void rowsum_publish(int csum, bool resum, TeamScratch* ts, int team,
+                                               int par) {
+  const int sum = __reduce_add_sync(0xffffffffu, csum);
+  const bool any = __any_sync(0xffffffffu, resum);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&ts->rs[team][par], sum);
+    if (any) atomicOr(&ts->rf[team][par], 1);
+  }
+}
+__device__ __forceinline__ int rowsum_collect(const uint8_t* crow, int64_t K, int W, int w,
+                                              TeamScratch* ts, int team, int par) {
+  if (ts->rf[team][par]) return team_code_sum(crow, K, W, w, ts, team);
+  return ts->rs[team][par];
+}
+__device__ __forceinline__ void rowsum_clear(TeamScratch* ts, int team, int par) {
+  ts->rs[team][par] = 0;
+  ts->rf[team][par] = 0;
 }
 
 // Code sum of the two int8-code chunks of a pair, re-read after a redecide
@@ -729,6 +756,8 @@ template <int N0, bool F32, int BITS, bool BULK, bool FULL>
 __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) {
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
+  griddep_launch();  // launched with PDL: the successor may queue behind us now
+  griddep_wait();    // ... and our predecessor has completed before any global access
   __shared__ TeamScratch ts;
   __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
   extern __shared__ __align__(128) uint8_t k1_ring[];
@@ -756,6 +785,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
         for (int s = 0; s < S; ++s) mbar_init(&full_bar[t][s], 1);
       mbar_init_fence();
     }
+    if (threadIdx.x < 16) (&ts.rs[0][0])[threadIdx.x] = (&ts.rf[0][0])[threadIdx.x] = 0;
     __syncthreads();
     if (leader) {
       for (int s = 0; s < S; ++s) {
@@ -803,6 +833,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       }
     }
     const float A32 = team_max_nan(lmax_nan, &ts, team, w, W);
+    if (W > 1 && leader && it > 0) rowsum_clear(&ts, team, (it - 1) & 1);  // read by all (barrier)
 
     // pathological rows (non-finite input, fp32 overflow) go the exact way
     const bool slow_row = !(A32 <= 3.0e38f);
@@ -923,10 +954,12 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       if (a.amax) a.amax[row] = amax_ref;  // exact max|y_ref| (outlier analysis)
     }
     if constexpr (BULK) {
+      if (a.rowsum && W > 1) rowsum_publish(csum, resum, &ts, team, it & 1);
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
       if (a.rowsum) {
-        const int sum = team_row_sum(csum, resum, crow, a.K, W, w, &ts, team);
+        const int sum = W == 1 ? team_row_sum(csum, resum, crow, a.K, 1, 0, &ts, team)
+                               : rowsum_collect(crow, a.K, W, w, &ts, team, it & 1);
         if (leader) a.rowsum[row] = sum;
       }
       if (leader) {
@@ -988,6 +1021,7 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
         for (int s = 0; s < S; ++s) mbar_init(&full_bar[t][s], 1);
       mbar_init_fence();
     }
+    if (threadIdx.x < 16) (&ts.rs[0][0])[threadIdx.x] = (&ts.rf[0][0])[threadIdx.x] = 0;
     __syncthreads();
     if (leader) {
       for (int s = 0; s < S; ++s) {
@@ -1043,6 +1077,7 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
 #pragma unroll
     for (int p = 1; p < P; ++p) lmax = max_nan(lmax, pmx[p]);
     const float A32 = team_max_nan(lmax, &ts, team, w, W);
+    if (W > 1 && leader && it > 0) rowsum_clear(&ts, team, (it - 1) & 1);  // read by all (barrier)
 
     // pathological rows (non-finite input, fp32 overflow) go the exact way
     const bool slow_row = !(A32 <= 3.0e38f);
@@ -1232,10 +1267,12 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
     if constexpr (BULK) {
       // every lane of the team is done with this stage: refill it with the
       // row `stages` ahead.
+      if (a.rowsum && W > 1) rowsum_publish(csum, resum, &ts, team, it & 1);
       if (W == 1) __syncwarp();
       else named_bar_sync(1 + team, W * 32);
       if (a.rowsum) {
-        const int sum = team_row_sum(csum, resum, crow, a.K, W, w, &ts, team);
+        const int sum = W == 1 ? team_row_sum(csum, resum, crow, a.K, 1, 0, &ts, team)
+                               : rowsum_collect(crow, a.K, W, w, &ts, team, it & 1);
         if (leader) a.rowsum[row] = sum;
       }
       if (leader) {
@@ -1380,9 +1417,9 @@ cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) 
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, threads, smem, st>>>(a);
+  cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(threads), smem, st, a);
   ++*launches;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int C, int N0, bool F32, int BITS>

@@ -238,12 +238,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = ss->tmem_base;
+  // PDL: the prologue above (barriers, TMEM allocation) overlapped the
+  // previous kernel's tail; no global memory is touched before this wait.
+  if (warp == 0 && lane == 0) {  // kernel parameters, not predecessor output
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+  }
+  griddep_launch();
+  griddep_wait();
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completions land on the leader) ========
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
       const uint32_t full0 = mapa(smem_u32(&ss->full[0]), 0);
       int s = 0;
       uint32_t ph = 0;
@@ -508,9 +514,10 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   const int tiles = v.ttiles * v.ctiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  kern<<<(unsigned)(2 * pairs), V3_THREADS, smem, st>>>(mw, mx, v);
+  const cudaError_t le = launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(V3_THREADS), smem, st,
+                                    mw, mx, v);
   ++*launches;
-  return cudaGetLastError();
+  return le;
 }
 
 }  // namespace crt
