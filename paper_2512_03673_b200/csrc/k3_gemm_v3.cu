@@ -59,8 +59,8 @@ struct V3Smem {
   uint64_t dec_full[4];   // leader: decompress warp's commit (A slot expanded)
   uint64_t dec_empty[4];  // leader: MMA commit (A slot consumed)
   uint32_t tmem_base;
-  float sa[2][V3_BT];     // per-token activation scale of the tile
-  int sums[2][V3_BT];     // per-token code sums
+  alignas(16) float sa[2][V3_BT];  // per-token activation scale of the tile (ld.shared.v4)
+  alignas(16) int sums[2][V3_BT];  // per-token code sums, x32
 };
 
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
@@ -179,6 +179,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 16-byte shared-memory broadcast load (every lane reads the same address).
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void lds_row32(uint32_t saddr, uint32_t (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 t = lds128(saddr + 16 * q);
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
 }
 
 struct V3Args {
@@ -378,10 +397,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         if (a.out_kind == 0) {
           __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(a.y) + m0 * a.ldy + n;
           if (jn == 32) {
+            // the chunk's 32 token scales / offsets as shared broadcasts
+            // (explicit ld.shared: the generic pointer compiles to LD.E)
+            uint32_t sav[32], smv[32];
+            lds_row32(smem_u32(sa), sav);
+            if constexpr (!W8) lds_row32(smem_u32(sm), smv);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int v = W8 ? (int)acc[j] : (((int)acc[j] - sm[j]) >> 2);
-              yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
+              const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
+              yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
             }
           } else {
 #pragma unroll
