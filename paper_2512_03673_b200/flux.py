@@ -20,7 +20,13 @@ input once) and run as ONE GEMM against the row-concatenated prepared
 weights (N = 9216 or 21504).  Every output channel depends only on its own
 weight row, scale and bias, and the activation codes / scales are the same,
 so the fused outputs are bit-identical to the separate ones
-(tests/test_flux_stack.py).  Attention, norms and activations are not part of
+(tests/test_flux_stack.py).
+
+Streams: a double block's text-stream linears (M = 512) are independent of
+its image-stream linears until the joint attention, and alone they fill
+less than half of the GPU; with ``streams=2`` they run on a second CUDA
+stream (own workspace) beside the image ones, joined at the end of the step.
+Same kernels, same results.  Attention, norms and activations are not part of
 the ConvLinear4bit path; the stack feeds each linear synthetic activations
 of the right shape.
 """
@@ -79,8 +85,9 @@ class FluxStack:
     either one layer per linear or fused per input group."""
 
     def __init__(self, linears: List[Linear], fused: bool, n0: int = 16, bits: int = 4,
-                 device="cuda", seed: int = 2):
+                 device="cuda", seed: int = 2, streams: int = 1):
         self.linears, self.fused, self.device = linears, fused, torch.device(device)
+        self.streams = streams
         self.spec = api.RotationSpec(api.RotationKind.regular, n0)
         self.q = api.QuantSpec(bits)
         groups: Dict[str, List[Linear]] = {}
@@ -109,14 +116,31 @@ class FluxStack:
                     torch.bfloat16)
         self.ws = api.Workspace(max(l.m for l in linears), max(l.k for l in linears),
                                 self.device)
+        if streams > 1:
+            self.side = torch.cuda.Stream(self.device)
+            self.ws_side = api.Workspace(max(l.m for l in linears), max(l.k for l in linears),
+                                         self.device)
         self.outputs = {id(u): torch.empty(u[0][0].m, u[1].out_features, dtype=torch.bfloat16,
                                            device=self.device) for u in self.units}
 
     def step(self) -> None:
+        if self.streams == 1:
+            for u in self.units:
+                ls, layer = u
+                x = self.inputs[(ls[0].m, ls[0].k)]
+                api.forward(x, layer, self.q, out="bf16", y=self.outputs[id(u)],
+                            workspace=self.ws)
+            return
+        main = torch.cuda.current_stream(self.device)
+        self.side.wait_stream(main)
         for u in self.units:
             ls, layer = u
             x = self.inputs[(ls[0].m, ls[0].k)]
-            api.forward(x, layer, self.q, out="bf16", y=self.outputs[id(u)], workspace=self.ws)
+            txt = ".txt." in ls[0].name
+            with torch.cuda.stream(self.side if txt else main):
+                api.forward(x, layer, self.q, out="bf16", y=self.outputs[id(u)],
+                            workspace=self.ws_side if txt else self.ws)
+        main.wait_stream(self.side)
 
     def output_of(self, name: str) -> Optional[torch.Tensor]:
         """The output columns of linear `name` (a view into its unit's output)."""

@@ -27,3 +27,16 @@ def test_fused_stack_bit_identical_to_unfused():
     torch.cuda.synchronize()
     for l in ls:
         assert torch.equal(a.output_of(l.name), b.output_of(l.name)), l.name
+
+
+@pytest.mark.gpu
+def test_two_stream_stack_bit_identical():
+    """Text-stream linears on a second CUDA stream give the same outputs."""
+    ls = flux_linears(double_blocks=2, single_blocks=1, m_img=160, m_txt=48, d=256, ff=1024)
+    a = FluxStack(ls, fused=True)
+    b = FluxStack(ls, fused=True, streams=2)
+    a.step()
+    b.step()
+    torch.cuda.synchronize()
+    for l in ls:
+        assert torch.equal(a.output_of(l.name), b.output_of(l.name)), l.name

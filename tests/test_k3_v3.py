@@ -20,7 +20,9 @@ def _unpack(c, k):
 
 
 SHAPES = [(1, 32, 16), (5, 96, 40), (7, 40, 24), (65, 100, 300), (193, 160, 257),
-          (384, 3072, 768), (257, 3104, 1000), (1024, 12288, 512), (4096, 3072, 3072)]
+          (384, 3072, 768), (257, 3104, 1000), (1024, 12288, 512), (4096, 3072, 3072),
+          # few tokens (FLUX AdaLN: M = 1, N = 18432)
+          (1, 3072, 18432), (8, 3072, 9216), (3, 12288, 3072), (2, 3104, 700), (8, 48, 33)]
 
 
 @pytest.mark.parametrize("M,K,N", SHAPES)

@@ -19,8 +19,8 @@ ap.add_argument("--n0", type=int, default=16)
 args = ap.parse_args()
 ls = flux_linears()
 ops = stack_ops(ls)
-for fused in (False, True):
-    st = FluxStack(ls, fused=fused, n0=args.n0)
+for fused, streams in ((False, 1), (True, 1), (True, 2)):
+    st = FluxStack(ls, fused=fused, n0=args.n0, streams=streams)
     for _ in range(2):
         st.step()
     torch.cuda.synchronize()
@@ -34,7 +34,8 @@ for fused in (False, True):
         ts.append(a.elapsed_time(b))
     ms = statistics.median(ts)
     print(json.dumps({"workload": "FLUX.1-dev linear stack 19 double + 38 single blocks (494 linears)",
-                      "fused_siblings": fused, "units": len(st.units), "n0": args.n0,
+                      "fused_siblings": fused, "cuda_streams": streams,
+                      "units": len(st.units), "n0": args.n0,
                       "ms_per_step": ms, "TOPS": ops / (ms * 1e-3) / 1e12,
                       "packed_weights_GiB": sum(l.n * ((l.k + 1) // 2) for l in ls) / 2**30}),
           flush=True)
