@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CRT_LIB_OVERRIDE") or os.path.join(HERE, "libconvrot_b200.so")  # override: dev A/B only
+LIB_PATH = os.path.join(HERE, "libconvrot_b200.so")
 
 # crt_status (errors.hpp:9-67 taxonomy)
 CRT_OK = 0

@@ -655,10 +655,7 @@ __device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], ui
       for (int q = 0; q < 4; ++q) {
         wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                              __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040), 0x5410);
-        if constexpr (BITS == 5) {
-          wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
-          csum = __dp4a((int)wds[q], 0x01010101, csum);
-        }
+        if constexpr (BITS == 5) csum = __dp4a((int)wds[q], 0x01010101, csum);
       }
       *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
     }
@@ -897,7 +894,9 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
       const float margin = (float)B * (inv * 1.05f) +
                            (float)(QMAX + 4) * 2.384185791015625e-7f + 1e-9f;
       const float thr = 0.5f - margin;
-      const float mg = __uint_as_float(kMagic23 + (BITS == 8 ? 0u : 8u));
+      // 4-bit packing wants the +8-biased magic (low nibble = code + 8); int8
+      // codes (BITS 5, 8) the plain one: the low byte IS the two's-complement code
+      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
       const float2 iv = make_float2(inv, inv);
       const float2 cc = make_float2(mg, mg);
 #pragma unroll 1
@@ -1171,7 +1170,9 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
       // code + 8 in [1, 15] with nothing above it: one IMAD packs a byte
       // (odd*16 + even) in offset binary and one XOR 0x88888888 per word
       // turns it into two's-complement nibbles.
-      const float mg = __uint_as_float(kMagic23 + (BITS == 8 ? 0u : 8u));
+      // 4-bit packing wants the +8-biased magic (low nibble = code + 8); int8
+      // codes (BITS 5, 8) the plain one: the low byte IS the two's-complement code
+      const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
       const float2 iv = make_float2(inv, inv);
       const float2 cc = make_float2(mg, mg);
 #pragma unroll
@@ -1211,10 +1212,7 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
               wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                                    __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040),
                                    0x5410);
-              if constexpr (BITS == 5) {
-                wds[q] = __vsub4(wds[q], 0x08080808u);  // code + 8 -> code
-                ps = __dp4a((int)wds[q], 0x01010101, ps);
-              }
+              if constexpr (BITS == 5) ps = __dp4a((int)wds[q], 0x01010101, ps);
             }
             *reinterpret_cast<uint4*>(crow + chunk * 16) =
                 make_uint4(wds[0], wds[1], wds[2], wds[3]);
