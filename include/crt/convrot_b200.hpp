@@ -140,6 +140,18 @@ inline PreparedLayer prepare_layer_shard(const void* w, DType dt, int64_t n, int
   return PreparedLayer(h);
 }
 
+// Row-parallel shard (SURVEY.md 8e "K", 8f row f3): input columns
+// [r*K/P, (r+1)*K/P) of the full layer's codes, full-K channel scales.
+inline PreparedLayer prepare_layer_kshard(const void* w, DType dt, int64_t n, int64_t k,
+                                          int64_t ldw, const float* bias,
+                                          const RotationSpec& rot, QuantSpec wq, int rank,
+                                          int nranks, void* stream = nullptr) {
+  crt_layer_desc d{n, k, rot.c(), wq.bits, static_cast<int32_t>(dt)};
+  crt_layer* h = nullptr;
+  check(crt_layer_prepare_kshard(&d, w, ldw, bias, rank, nranks, stream, &h));
+  return PreparedLayer(h);
+}
+
 // ---- forward workspace (no hidden allocation on the forward path) --------
 class Workspace {
  public:
@@ -161,6 +173,47 @@ inline void quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scale
                        void* stream = nullptr) {
   check(crt_quant_gemm(a_codes, lda, a_scales, aq.bits, layer.handle(), m,
                        static_cast<int32_t>(out), y, ldy, stream));
+}
+
+// W4A4 fast path pieces: K1 with int8-stored codes + per-row code sums, and
+// the hardware-expansion GEMM (K3 v3) that consumes them.
+inline void rotate_quantize_i8(const void* x, DType dt, int64_t m, int64_t k, int64_t ldx,
+                               const RotationSpec& rot, uint8_t* codes, int64_t ld_codes,
+                               float* scales_f32, int32_t* code_sums, void* stream = nullptr) {
+  const crt_rotation_spec r = rot.c();
+  check(crt_rotate_quant_i8(x, static_cast<int32_t>(dt), m, k, ldx, &r, codes, ld_codes,
+                            scales_f32, code_sums, stream));
+}
+inline void quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+                          const int32_t* code_sums, const PreparedLayer& layer, int64_t m,
+                          Out out, void* y, int64_t ldy, void* stream = nullptr) {
+  check(crt_quant_gemm_i8(a_codes, lda, a_scales, code_sums, layer.handle(), m,
+                          static_cast<int32_t>(out), y, ldy, stream));
+}
+
+// Row-parallel pieces: K1 with the global per-row max (after a MAX
+// all-reduce of every rank's crt_rotated_row_absmax), and the dequant of the
+// SUM-all-reduced int32 accumulators.
+inline void rotated_row_absmax(const void* x, DType dt, int64_t m, int64_t k, int64_t ldx,
+                               const RotationSpec& rot, double* amax_rows,
+                               void* stream = nullptr) {
+  const crt_rotation_spec r = rot.c();
+  check(crt_rotated_row_absmax(x, static_cast<int32_t>(dt), m, k, ldx, &r, amax_rows, stream));
+}
+inline void rotate_quantize_amax(const void* x, DType dt, int64_t m, int64_t k, int64_t ldx,
+                                 const RotationSpec& rot, const double* amax_rows, QuantSpec aq,
+                                 uint8_t* codes, int64_t ld_codes, float* scales_f32,
+                                 double* scales_f64, int32_t* code_sums,
+                                 void* stream = nullptr) {
+  const crt_rotation_spec r = rot.c();
+  check(crt_rotate_quant_amax(x, static_cast<int32_t>(dt), m, k, ldx, &r, amax_rows, aq.bits,
+                              codes, ld_codes, scales_f32, scales_f64, code_sums, stream));
+}
+inline void dequant(const int32_t* acc, int64_t ld_acc, int64_t m, const float* a_scales,
+                    const PreparedLayer& layer, Out out, void* y, int64_t ldy,
+                    void* stream = nullptr) {
+  check(crt_dequant(acc, ld_acc, m, a_scales, layer.handle(), static_cast<int32_t>(out), y, ldy,
+                    stream));
 }
 
 // forward(x, layer, aq) on device buffers: K1 then K3.

@@ -4,6 +4,7 @@
 //   test_host_api cpu | gpu
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -114,6 +115,55 @@ static void gpu_tests() {
   // int_gemm capacity precheck (pipeline.cpp:184-192) is host-side
   EXPECT(throws<cb::InvalidValueError>([&] {
     cb::forward(x2, cb::DType::f32, M, K, L2, cb::QuantSpec{5}, cb::Out::f32, y2, N, ws2);
+  }));
+  // row-parallel (K-sharded) forward, P = 2 shards run one after the other:
+  // global row max, per-shard K1 + int32 partial GEMM, summed, dequant ==
+  // the unsharded forward bit for bit
+  for (int i = 0; i < M * K; ++i) x[i] = (float)((i * 29) % 17) - 8.f;
+  cudaMemcpy(x2, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
+  float* yref;
+  cudaMalloc(&yref, M * N * 4);
+  cb::forward(x2, cb::DType::f32, M, K, L2, cb::QuantSpec{4}, cb::Out::f32, yref, N, ws2);
+  const int P = 2, Ks = K / P;
+  double *am, *am_s;
+  float *sa;
+  int32_t *acc, *part, *sums;
+  uint8_t* codes;
+  cudaMalloc(&am, M * 8);
+  cudaMalloc(&am_s, M * 8);
+  cudaMalloc(&sa, M * 4);
+  cudaMalloc(&acc, M * N * 4);
+  cudaMalloc(&part, M * N * 4);
+  cudaMalloc(&sums, M * 4);
+  cudaMalloc(&codes, M * 64);
+  std::vector<double> amax(M, 0.0), part_amax(M);
+  for (int r = 0; r < P; ++r) {  // exact local maxima, MAX-reduced on the host here
+    cb::rotated_row_absmax(x2 + r * Ks, cb::DType::f32, M, Ks, K, reg, am_s);
+    cudaMemcpy(part_amax.data(), am_s, M * 8, cudaMemcpyDeviceToHost);
+    for (int m = 0; m < M; ++m) amax[m] = std::max(amax[m], part_amax[m]);
+  }
+  cudaMemcpy(am, amax.data(), M * 8, cudaMemcpyHostToDevice);
+  std::vector<int32_t> total(M * N, 0), p(M * N);
+  cb::PreparedLayer shard0 = cb::prepare_layer_kshard(w2, cb::DType::f32, N, K, K, b2, reg,
+                                                      cb::QuantSpec{4}, 0, P);
+  for (int r = 0; r < P; ++r) {
+    cb::PreparedLayer sh = cb::prepare_layer_kshard(w2, cb::DType::f32, N, K, K, b2, reg,
+                                                    cb::QuantSpec{4}, r, P);
+    cb::rotate_quantize_amax(x2 + r * Ks, cb::DType::f32, M, Ks, K, reg, am, cb::QuantSpec{4},
+                             codes, 64, sa, nullptr, sums);
+    cb::quant_gemm_i8(codes, 64, sa, sums, sh, M, cb::Out::i32_acc, part, N);
+    cudaMemcpy(p.data(), part, M * N * 4, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < M * N; ++i) total[i] += p[i];
+  }
+  cudaMemcpy(acc, total.data(), M * N * 4, cudaMemcpyHostToDevice);
+  cb::dequant(acc, N, M, sa, shard0, cb::Out::f32, y2, N);
+  cudaDeviceSynchronize();
+  std::vector<float> yr(M * N), yt(M * N);
+  cudaMemcpy(yr.data(), yref, M * N * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(yt.data(), y2, M * N * 4, cudaMemcpyDeviceToHost);
+  EXPECT(std::memcmp(yr.data(), yt.data(), M * N * 4) == 0);
+  EXPECT(throws<cb::ShapeError>([&] {  // 64 / 3 shards do not divide K
+    cb::prepare_layer_kshard(w2, cb::DType::f32, N, K, K, b2, reg, cb::QuantSpec{4}, 0, 3);
   }));
 }
 
