@@ -11,6 +11,7 @@ timeout 600 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" >> $OUT/be
 timeout 600 python bench.py --path v2 --no-cpu-baseline --no-e2e > $OUT/bench_v2.log 2>&1
 timeout 900 python tools/flux_stack.py > $OUT/flux_stack.jsonl 2>&1
 timeout 300 python tools/k1_time.py > $OUT/k1_time.log 2>&1
+timeout 300 python tools/n0_sweep.py > $OUT/n0_sweep.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --profile > $OUT/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_v3 -s 2 -c 1 \
