@@ -37,12 +37,16 @@ namespace crt {
 namespace {
 
 constexpr int V3_BM = 128;         // channels per CTA (pair: 256)
-constexpr int V3_BT = 192;         // tokens per pair tile
+constexpr int V3_BT = 192;         // tokens per pair tile (measured: 160 and 224 both ~20% slower)
 constexpr int V3_BTH = V3_BT / 2;  // token rows of B per CTA
 constexpr int V3_PS = 7;           // smem stages
 constexpr int V3_THREADS = 384;
 constexpr int V3_A_STAGE = V3_BM * 128;  // 16 KB: 128 rows x (8 x 16 B padded units)
 constexpr int V3_B_STAGE = V3_BTH * 128; // 12 KB int8
+// TMEM (512 columns): two V3_BT-column accumulators at 0 and 256, the rest of
+// each half holds 32-column A slots (one 128-code K block each)
+constexpr int V3_SLOTS = (256 - V3_BT) / 32 * 2;
+static_assert(V3_SLOTS >= 2, "no TMEM room for A slots");
 constexpr int V3_STAGE = V3_A_STAGE + V3_B_STAGE;
 // transaction bytes of one stage: a 16U4_ALIGN16B box completes its PACKED
 // data bytes (64 per row), not its padded smem footprint (128 per row) --
@@ -56,8 +60,8 @@ struct V3Smem {
   uint64_t empty[V3_PS];  // both: MMA commit multicast
   uint64_t acc_full[2];   // both: MMA commit multicast
   uint64_t acc_empty[2];  // leader: 8 epilogue warps x 2 CTAs
-  uint64_t dec_full[4];   // leader: decompress warp's commit (A slot expanded)
-  uint64_t dec_empty[4];  // leader: MMA commit (A slot consumed)
+  uint64_t dec_full[V3_SLOTS];   // leader: decompress warp's commit (A slot expanded)
+  uint64_t dec_empty[V3_SLOTS];  // leader: MMA commit (A slot consumed)
   uint32_t tmem_base;
   alignas(16) float sa[2][V3_BT];  // per-token activation scale of the tile (ld.shared.v4)
   alignas(16) int sums[2][V3_BT];  // per-token code sums, x32
@@ -65,7 +69,8 @@ struct V3Smem {
 
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
 __device__ __forceinline__ uint32_t a_col(int s) {
-  return (s < 2 ? 192u : 448u) + (uint32_t)(s & 1) * 32u;
+  constexpr int H = V3_SLOTS / 2;
+  return (s < H ? (uint32_t)V3_BT : 256u + (uint32_t)V3_BT) + (uint32_t)(s % H) * 32u;
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -241,7 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
       mbar_init(&ss->acc_full[b], 1);
       mbar_init(&ss->acc_empty[b], 16);
     }
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < V3_SLOTS; ++b) {
       mbar_init(&ss->dec_full[b], 1);
       mbar_init(&ss->dec_empty[b], 1);
     }
@@ -317,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
             s = 0;
             ph ^= 1;
           }
-          if (++slot == 4) {
+          if (++slot == V3_SLOTS) {
             slot = 0;
             sph ^= 1;
           }
@@ -352,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
             s = 0;
             ph ^= 1;
           }
-          if (++slot == 4) {
+          if (++slot == V3_SLOTS) {
             slot = 0;
             sph ^= 1;
           }
