@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n0", type=int, default=N0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=6.0,
+                    help="--impl reference: CPU seconds per step (bounded sample of the rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--path", choices=["v3", "v2"], default="v3",
@@ -121,7 +123,7 @@ def run_reference_arm(args):
         return  # N>1: rank 0 alone runs and prints
     threads = os.cpu_count() or 1
     ref = CpuReference(threads)
-    rows = ref.calibrate(target_s=6.0, max_rows=1024)
+    rows = ref.calibrate(target_s=args.ref_seconds, max_rows=1024)
     for _ in range(args.warmup):
         ref.step(rows)
     times = [ref.step(rows) for _ in range(args.steps)]
@@ -134,7 +136,8 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int4", "data": "synthetic (seeded gaussian, bf16-representable)",
-        "config": {"workload": WORKLOAD, "rows_per_step": rows, "n0": N0},
+        "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
+                   "n0": N0, "bits": "W4A4", "rows_per_step": rows},
         "cpu_baseline": {"value": v, "unit": "TOPS", "cores": ref.threads, "kind": ref.kind,
                          "sample": sample},
         "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
