@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k3_gemm.h"
@@ -171,6 +172,19 @@ __device__ __forceinline__ void tc_mma_pair_ts(uint32_t tmem_d, uint32_t tmem_a,
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// A from shared memory (SS form): W8A8 needs no expansion, so its int8
+// weight tile feeds the MMA straight from the TMA stage.
+__device__ __forceinline__ void tc_mma_pair_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -215,6 +229,7 @@ struct V3Args {
   int32_t out_kind;  // 0 bf16, 1 f32, 2 int32 accumulators
   void* y;
   int64_t ldy;
+  int32_t w8_ss;     // W8A8: A straight from shared memory (no TMEM copy)
 };
 
 // W8 = false: W4A4 (offset-binary int4 weights, hardware expansion);
@@ -308,6 +323,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         tc_fence_after();
         const uint32_t dcol = tmem + acc_col(ab);
         for (int kb = 0; kb < KB; ++kb) {
+          if (W8 && a.w8_ss) {  // W8A8, SS form: both operands from the stage
+            mbar_wait(&ss->full[s], ph);
+            tc_fence_after();
+            const uint32_t abase = smem_u32(stg + s * V3_STAGE);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_pair_ss(dcol, sw128_desc(abase + kk * 32),
+                             sw128_desc(abase + V3_A_STAGE + kk * 32), idesc,
+                             (kb | kk) != 0 ? 1u : 0u);
+            tc_commit_pair(&ss->empty[s]);
+            if (++s == V3_PS) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           mbar_wait(&ss->dec_full[slot], sph);  // A expanded (implies the stage landed)
           tc_fence_after();
           const uint32_t bbase = smem_u32(stg + s * V3_STAGE) + V3_A_STAGE;
@@ -337,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
   } else if (warp == 3) {
     // ===== decompress issuer (leader): padded int4 smem -> int8 TMEM ========
     // A separate issuing thread, so the copies can run beside the MMAs.
-    if (leader && lane == 0) {
+    if (leader && lane == 0 && !(W8 && a.w8_ss)) {
       int s = 0, slot = 0;
       uint32_t ph = 0, sph = 0;
       for (int t = pair; t < ntiles; t += npairs) {
@@ -531,6 +562,11 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.out_kind = a.out_kind;
   v.y = a.y;
   v.ldy = a.ldy;
+  static const bool w8_ts = [] {  // A/B switch: W8A8 through the TMEM copy path
+    const char* e = getenv("CRT_K3_W8_TS");
+    return e && e[0] == '1';
+  }();
+  v.w8_ss = w8 && !w8_ts;
   const size_t smem = 1024 + V3_PS * V3_STAGE + sizeof(V3Smem);
   auto kern = w8 ? k3_v3_kernel<true> : k3_v3_kernel<false>;
   static bool attr[2] = {false, false};
