@@ -1,6 +1,8 @@
 """Parity of the opt-in kernel paths, run in a subprocess by
-tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K3_V1=1 set before the
-library loads (the switches are read once per process)."""
+tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K1_FAST=1 / CRT_K3_V1=1 /
+CRT_K3_W8_TS=1 set before the library loads (the switches are read once per
+process).  W4A4 against the oracle; W8A8 accumulators against the exact
+integer GEMM of the exported codes."""
 import sys
 
 import numpy as np
@@ -32,6 +34,19 @@ def main():
                                       O.pack_int4_rows(f["act_codes"])), (n0, fam, m, k)
                 assert np.array_equal(s64.cpu().numpy(), f["act_scales"]), (n0, fam, m, k)
                 assert np.array_equal(acc.cpu().numpy(), f["acc"]), (n0, fam, m, k)
+    # W8A8 (f1): the v3 SS / TMEM-copy / v1 GEMMs against the exact integer GEMM
+    q8 = QuantSpec(8)
+    for (m, k, n) in ((97, 3072, 300), (193, 12288, 256)):
+        x = to_t(O.synth_input(m, k, "colwise", 31))
+        w = to_t(O.synth_input(n, k, "gaussian", 32))
+        spec = RotationSpec(RotationKind.regular, 16)
+        layer = crt.prepare_layer(w, None, spec, q8)
+        codes, sa = crt.rotate_quantize(x, spec, q8)
+        a8 = codes[:, :k].view(torch.int8).to(torch.float64)
+        b8 = layer.export(scales64=False)[0][:, :k].view(torch.int8).to(torch.float64)
+        ref = (a8 @ b8.T).round().to(torch.int64)
+        got = crt.forward(x, layer, q8, out="i32").to(torch.int64)
+        assert torch.equal(got, ref), ("w8a8", m, k, n)
     print("ok")
 
 
