@@ -5,6 +5,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
+#include <mutex>
+
 namespace crt {
 
 enum : int { kRotNone = 0, kRotSylvester = 1, kRotRegular = 2 };
@@ -129,6 +132,47 @@ __device__ __forceinline__ bool regular_negative(uint32_t k, uint32_t j) {
 // Sylvester (hadamard.cpp:70-89): H[k][j] = (-1)^popcount(k & j).
 __device__ __forceinline__ bool sylvester_negative(uint32_t k, uint32_t j) {
   return (__popc(k & j) & 1u) != 0;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launch helpers, safe for concurrent callers and several devices
+// in one process (layer handles may be used from many threads, convlinear4bit.h).
+// ---------------------------------------------------------------------------
+constexpr int kMaxDevices = 64;
+
+inline int device_sm_count() {
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = cache[dev % kMaxDevices];
+  int v = slot.load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    slot.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// Per (kernel, device): the largest dynamic shared-memory size requested so
+// far.  The attribute only ever grows (under the mutex), so a concurrent
+// caller can never lower a limit another launch relies on.
+struct SmemAttr {
+  std::atomic<size_t> granted[kMaxDevices];
+  std::mutex mu;
+};
+template <typename Kernel>
+inline cudaError_t ensure_dyn_smem(Kernel kern, size_t bytes, SmemAttr& c, bool max_carveout) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<size_t>& g = c.granted[dev % kMaxDevices];
+  if (g.load(std::memory_order_acquire) >= bytes) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (g.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && max_carveout)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) g.store(bytes, std::memory_order_release);
+  return e;
 }
 
 // ---------------------------------------------------------------------------

@@ -1365,12 +1365,7 @@ cudaError_t k1_exact_launch(const K1Args& a, cudaStream_t st);
 
 template <int N0, bool F32, int BITS>
 cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   K1Args a = a0;
   const int W = a.team_warps;
   const size_t rb = (size_t)a.K * (F32 ? 4 : 2);
@@ -1398,15 +1393,9 @@ cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) 
   const bool full = a.K / 16 == (int64_t)a.chunks * W * 32;
   auto kern = full ? k1_rolled<N0, F32, BITS, true, true> : k1_rolled<N0, F32, BITS, true, false>;
   if (bulk) {
-    static size_t smem_set[2] = {0, 0};  // per instantiation, [full]
-    if (smem > smem_set[full]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-      smem_set[full] = smem;
-    }
+    static SmemAttr attr[2];  // per instantiation, [full]
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[full], true);
+    if (e != cudaSuccess) return e;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
@@ -1422,12 +1411,7 @@ cudaError_t launch_rolled(const K1Args& a0, cudaStream_t st, int64_t* launches) 
 
 template <int C, int N0, bool F32, int BITS>
 cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   K1Args a = a0;
   const int W = a.team_warps;
   const size_t rb = (size_t)a.K * (F32 ? 4 : 2);
@@ -1449,15 +1433,9 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   const bool full = a.K / 16 == (int64_t)C * W * 32;  // every lane owns C whole chunks
   auto kern = full ? k1_fast<C, N0, F32, BITS, true, true> : k1_fast<C, N0, F32, BITS, true, false>;
   {
-    static size_t smem_set[2] = {0, 0};  // per instantiation, [full]
-    if (smem > smem_set[full]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-      smem_set[full] = smem;
-    }
+    static SmemAttr attr[2];  // per instantiation, [full]
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[full], true);
+    if (e != cudaSuccess) return e;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);

@@ -372,12 +372,7 @@ namespace crt {
 
 template <int N0, int BITS>
 cudaError_t launch_mma(const K1Args& a0, cudaStream_t st, int64_t* launches) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   K1Args a = a0;
   const int ntiles = (int)(a.K / 256);
   int W = (ntiles + 11) / 12;  // ~12 tiles (3072 elements) per warp per row
@@ -396,20 +391,26 @@ cudaError_t launch_mma(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   const int threads = teams * W * 32;
   const size_t smem = (size_t)teams * S * rb;
   auto kern = k1_mma<N0, BITS>;
-  static bool table = false;  // per (N0, BITS) instantiation; idempotent
-  if (!table) {
-    k1_mma_table_init<N0><<<1, 32, 0, st>>>();
-    ++*launches;
-    table = true;
+  {  // the device-side fragment table, once per device (complete before use)
+    static std::atomic<bool> table[kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!table[dev % kMaxDevices].load(std::memory_order_acquire)) {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!table[dev % kMaxDevices].load(std::memory_order_relaxed)) {
+        k1_mma_table_init<N0><<<1, 32, 0, st>>>();
+        ++*launches;
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        table[dev % kMaxDevices].store(true, std::memory_order_release);
+      }
+    }
   }
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  static SmemAttr attr;
+  {
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr, true);
     if (e != cudaSuccess) return e;
-    smem_set = smem;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);

@@ -562,12 +562,7 @@ bool k3_v2_supported(const K3Args& a) {
 }
 
 cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   CUtensorMap ma, mb;
   const int64_t kbytes = (a.K + 1) / 2;
   if (!make_codes_map(&ma, a.a_codes, a.M, kbytes, a.lda, V2_BM) ||
@@ -586,12 +581,10 @@ cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.y = a.y;
   v.ldy = a.ldy;
   const size_t smem = 1024 + V2_PS * V2_PK_STAGE + V2_KS * V2_B8_STAGE + sizeof(V2Smem);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k3_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static SmemAttr attr;
+  {
+    const cudaError_t e = ensure_dyn_smem(k3_v2_kernel, smem, attr, false);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int tiles = v.mtiles * v.ntiles;
   int pairs = num_sms / 2;

@@ -511,12 +511,7 @@ bool k3_v3_supported(const K3Args& a) {
 }
 
 cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int num_sms = device_sm_count();
   auto fn = encode_fn_v3();
   CUtensorMap mw, mx;
   const bool w8 = a.bits == 8;
@@ -569,12 +564,10 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.w8_ss = w8 && !w8_ts;
   const size_t smem = 1024 + V3_PS * V3_STAGE + sizeof(V3Smem);
   auto kern = w8 ? k3_v3_kernel<true> : k3_v3_kernel<false>;
-  static bool attr[2] = {false, false};
-  if (!attr[w8]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static SmemAttr attr[2];
+  {
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[w8], false);
     if (e != cudaSuccess) return e;
-    attr[w8] = true;
   }
   const int tiles = v.ttiles * v.ctiles;
   int pairs = num_sms / 2;
