@@ -240,3 +240,33 @@ def test_launch_counter_moves():
     crt.rotate_quantize(torch.randn(4, 256, device=DEV).to(torch.bfloat16),
                         RotationSpec(RotationKind.regular, 16))
     assert crt.launch_count() > before
+
+
+# ---------------------------------------------------------------------------
+# Full-size forward, row-sampled oracle: scales are per token,
+# so the reference's forward on a row subset X[S, :] is exactly rows S of the
+# full result.  The oracle prepares the FULL weights itself; the GPU runs the
+# full-size forward (the production path: K1 int8 codes + K3 v3).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("M,K,N,n0,family", [
+    (4096, 3072, 3072, 16, "colwise"),     # configs[0] attn-proj
+    (4608, 3072, 12288, 16, "gaussian"),   # configs[1] fc1
+    (4608, 12288, 3072, 16, "rowwise"),    # configs[1] fc2
+    (4608, 15360, 3072, 16, "colwise"),    # configs[3] single-block proj_out
+    (4608, 3072, 3072, 256, "colwise"),    # configs[2] N0 sweep, largest group
+])
+def test_forward_full_size_row_sampled_vs_oracle(M, K, N, n0, family):
+    xb = O.synth_input(M, K, family, 41)
+    wb = O.synth_input(N, K, "gaussian", 42)
+    bias = O.from_bf16_bits(O.to_bf16_bits(O.gaussian_matrix(1, N, 43)[0]))
+    spec = RotationSpec(RotationKind.regular, n0)
+    layer = crt.prepare_layer(bf16_tensor(wb), torch.from_numpy(bias).float().to(DEV), spec)
+    x = bf16_tensor(xb)
+    acc = crt.forward(x, layer, QuantSpec(4), out="i32").cpu().numpy()
+    y32 = crt.forward(x, layer, QuantSpec(4), out="f32").cpu().numpy().astype(np.float64)
+    rows = np.unique(np.concatenate([np.linspace(0, M - 1, 40).astype(np.int64), [1, M - 2]]))
+    wc, ws = O.prepare_layer(O.from_bf16_bits(wb), O.ROT_REGULAR, n0)
+    f = O.forward(O.from_bf16_bits(xb[rows]), wc, ws, bias, O.ROT_REGULAR, n0)
+    assert np.array_equal(acc[rows], f["acc"])
+    want = f["values"]
+    assert (np.abs(y32[rows] - want) <= 1e-6 * np.abs(want) + 1e-6).all()
