@@ -178,18 +178,24 @@ __device__ __noinline__ double y_exact_chunk(const void* row, int64_t chunk, int
       }
     }
   }
+  // Exponent span of the group's nonzero inputs from two integer reductions
+  // on the magnitude bits: |x| bits - 1 (unsigned) sends zeros to the top,
+  // so the minimum is the smallest nonzero magnitude; a maximum at or above
+  // the inf pattern means inf/NaN, a nonzero minimum below the smallest
+  // normal means a subnormal (both: not certified).
   const int g0 = e & ~(N0 - 1);
-  int emin = 1 << 20, emax = -1, bad = 0;
+  uint32_t bmax = 0u, bmin1 = 0xFFFFFFFFu;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const int ex = (int)((__float_as_uint(x[i]) >> 23) & 0xFFu);
-    const bool in = (i & ~(N0 - 1)) == g0 && x[i] != 0.f;
-    bad |= (in && (ex == 0 || ex == 255)) ? 1 : 0;
-    emin = in ? min(emin, ex) : emin;
-    emax = in ? max(emax, ex) : emax;
+    if ((i & ~(N0 - 1)) != g0) continue;  // compile-time for N0 == 16
+    const uint32_t b = __float_as_uint(x[i]) & 0x7FFFFFFFu;
+    bmax = max(bmax, b);
+    bmin1 = min(bmin1, b - 1u);
   }
+  const bool bad = bmax >= 0x7F800000u || (bmax != 0u && bmin1 + 1u < 0x00800000u);
+  const int emax = (int)(bmax >> 23), emin = (int)((bmin1 + 1u) >> 23);
   constexpr int L2 = N0 == 4 ? 2 : 4;
-  if (!bad && kind == kRotRegular && (emax < 0 || 1 + L2 + (emax - emin) + (F32 ? 24 : 8) <= 24))
+  if (!bad && kind == kRotRegular && (bmax == 0u || 1 + L2 + (emax - emin) + (F32 ? 24 : 8) <= 24))
     return (double)y32 * (N0 == 4 ? 0.5 : 0.25);
   return y_ref<F32>(row, j, N0, kind, rot_cols);
 }
@@ -395,6 +401,9 @@ template <bool F32, bool SMEM, bool FULL = false>
 __device__ __forceinline__ void load_pair(float2 (&v)[16], const void* rowp, int64_t c0,
                                           int64_t cstride, int64_t nchunks) {
   constexpr int CB = F32 ? 64 : 32;  // input bytes per chunk
+  // shared row copies are addressed in the 32-bit shared window: one cvta per
+  // pair, 32-bit offsets (the row is < 64 KB)
+  const uint32_t sbase = SMEM ? smem_u32(rowp) + (uint32_t)c0 * CB : 0u;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t chunk = c0 + h * cstride;
@@ -406,7 +415,7 @@ __device__ __forceinline__ void load_pair(float2 (&v)[16], const void* rowp, int
     if (FULL || chunk < nchunks) {
       const char* src = reinterpret_cast<const char*>(rowp) + chunk * CB;
       if constexpr (SMEM) {
-        const uint32_t sa = smem_u32(src);
+        const uint32_t sa = sbase + (uint32_t)(h * cstride) * CB;
 #pragma unroll
         for (int j = 0; j < CB / 16; ++j) {
           const uint4 t = ld_shared_v4(sa + j * 16);
@@ -466,13 +475,11 @@ __device__ __forceinline__ void rotate_pair(float2 (&v)[16]) {
 }
 
 __device__ __forceinline__ float pair_absmax(const float2 (&v)[16]) {
-  float m0 = 0.f, m1 = 0.f;
+  // four independent chains of depth 4 (not two of depth 8)
+  float m[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int i = 0; i < 16; i += 2) {
-    m0 = max3_abs(v[i].x, v[i].y, m0);
-    m1 = max3_abs(v[i + 1].x, v[i + 1].y, m1);
-  }
-  return max_nan(m0, m1);
+  for (int i = 0; i < 16; ++i) m[i & 3] = max3_abs(v[i].x, v[i].y, m[i & 3]);
+  return max_nan(max_nan(m[0], m[1]), max_nan(m[2], m[3]));
 }
 
 // ---- out-of-line cold paths (kept out of the hot loop) ---------------------
@@ -652,11 +659,12 @@ __device__ __forceinline__ void store_codes_pair(const uint32_t (&tb)[2][16], ui
     } else {
       uint32_t wds[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4; ++q)
         wds[q] = __byte_perm(__byte_perm(tb[h][4 * q], tb[h][4 * q + 1], 0x0040),
                              __byte_perm(tb[h][4 * q + 2], tb[h][4 * q + 3], 0x0040), 0x5410);
-        if constexpr (BITS == 5) csum = __dp4a((int)wds[q], 0x01010101, csum);
-      }
+      if constexpr (BITS == 5)  // two independent DP4A chains per chunk
+        csum += __dp4a((int)wds[0], 0x01010101, __dp4a((int)wds[1], 0x01010101, 0)) +
+                __dp4a((int)wds[2], 0x01010101, __dp4a((int)wds[3], 0x01010101, 0));
       *reinterpret_cast<uint4*>(crow + chunk * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
     }
   }
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   griddep_launch();  // launched with PDL: the successor may queue behind us now
-  griddep_wait();    // ... and our predecessor has completed before any global access
+  if constexpr (!BULK) griddep_wait();  // predecessor complete before any global access
   __shared__ TeamScratch ts;
   __shared__ uint64_t full_bar[kK1MaxTeams][kK1MaxStages];
   extern __shared__ __align__(128) uint8_t k1_ring[];
@@ -784,6 +792,7 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
     }
     if (threadIdx.x < 16) (&ts.rs[0][0])[threadIdx.x] = (&ts.rf[0][0])[threadIdx.x] = 0;
     __syncthreads();
+    griddep_wait();  // the shared-memory prologue above overlaps the predecessor's tail
     if (leader) {
       for (int s = 0; s < S; ++s) {
         const int64_t r = row0 + (int64_t)s * row_step;
@@ -803,9 +812,12 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
                                         (double)N0 * sqrtn * 2.220446049250313e-16;
 
   int it = 0;
-  for (int64_t row = row0; row < a.M; row += row_step, ++it) {
-    const int stage = BULK ? it % S : 0;
-    if constexpr (BULK) mbar_wait(&full_bar[team][stage], (uint32_t)((it / S) & 1));
+  int stage = 0;       // it % S, kept incrementally (no integer division per row)
+  uint32_t phase = 0;  // (it / S) & 1
+  for (int64_t row = row0; row < a.M;
+       row += row_step, ++it, stage = (stage + 1 == S) ? 0 : stage + 1,
+               phase ^= (stage == 0) ? 1u : 0u) {
+    if constexpr (BULK) mbar_wait(&full_bar[team][stage], phase);
     const void* rowp =
         BULK ? static_cast<const void*>(ring + (size_t)stage * row_bytes)
              : static_cast<const void*>(reinterpret_cast<const char*>(a.x) + row * a.ldx * esz);
@@ -1022,6 +1034,7 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
     }
     if (threadIdx.x < 16) (&ts.rs[0][0])[threadIdx.x] = (&ts.rf[0][0])[threadIdx.x] = 0;
     __syncthreads();
+    griddep_wait();  // the shared-memory prologue above overlaps the predecessor's tail
     if (leader) {
       for (int s = 0; s < S; ++s) {
         const int64_t r = row0 + (int64_t)s * row_step;
@@ -1041,9 +1054,12 @@ __global__ void __launch_bounds__(kK1FThreads, k1_fast_min_blocks(C)) k1_fast(K1
                                         (double)N0 * sqrtn * 2.220446049250313e-16;
 
   int it = 0;
-  for (int64_t row = row0; row < a.M; row += row_step, ++it) {
-    const int stage = BULK ? it % S : 0;
-    if constexpr (BULK) mbar_wait(&full_bar[team][stage], (uint32_t)((it / S) & 1));
+  int stage = 0;       // it % S, kept incrementally (no integer division per row)
+  uint32_t phase = 0;  // (it / S) & 1
+  for (int64_t row = row0; row < a.M;
+       row += row_step, ++it, stage = (stage + 1 == S) ? 0 : stage + 1,
+               phase ^= (stage == 0) ? 1u : 0u) {
+    if constexpr (BULK) mbar_wait(&full_bar[team][stage], phase);
     const void* rowp =
         BULK ? static_cast<const void*>(ring + (size_t)stage * row_bytes)
              : static_cast<const void*>(reinterpret_cast<const char*>(a.x) + row * a.ldx * esz);
