@@ -482,6 +482,54 @@ __device__ __forceinline__ float pair_absmax(const float2 (&v)[16]) {
   return max_nan(max_nan(m[0], m[1]), max_nan(m[2], m[3]));
 }
 
+// Per-chunk maxima of a pair: mx over chunk0 (.x), my over chunk1 (.y).
+// Same FMNMX3 count as pair_absmax; lets the row-max candidates be tracked
+// per chunk instead of per pair.
+__device__ __forceinline__ void pair_absmax2(const float2 (&v)[16], float& mx, float& my) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i & 1] = max3_abs(v[2 * i].x, v[2 * i + 1].x, a[i & 1]);
+    a[2 + (i & 1)] = max3_abs(v[2 * i].y, v[2 * i + 1].y, a[2 + (i & 1)]);
+  }
+  mx = max_nan(a[0], a[1]);
+  my = max_nan(a[2], a[3]);
+}
+
+// Exponent-span certificate of one bf16 chunk (16 inputs, the same test as
+// y_exact_chunk, over the whole chunk, so for N0 = 4 it is conservative):
+// true => every fp32 partial sum of the chunk's groups is exact, so each
+// y32 * rk IS the reference's double value.  Packed 16-bit SIMD min/max on
+// the bf16 magnitudes (zeros sent to 0xFFFF by the -1).
+template <int N0, bool SMEM>
+__device__ __forceinline__ bool chunk_certified_bf16(const void* rowp, int64_t chunk) {
+  uint32_t u[8];
+  if constexpr (SMEM) {
+    const uint32_t sa = smem_u32(rowp) + (uint32_t)chunk * 32u;
+    const uint4 t0 = ld_shared_v4(sa), t1 = ld_shared_v4(sa + 16);
+    u[0] = t0.x; u[1] = t0.y; u[2] = t0.z; u[3] = t0.w;
+    u[4] = t1.x; u[5] = t1.y; u[6] = t1.z; u[7] = t1.w;
+  } else {
+    const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(rowp) + chunk * 32);
+    const uint4 t0 = q[0], t1 = q[1];
+    u[0] = t0.x; u[1] = t0.y; u[2] = t0.z; u[3] = t0.w;
+    u[4] = t1.x; u[5] = t1.y; u[6] = t1.z; u[7] = t1.w;
+  }
+  uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t m = u[i] & 0x7FFF7FFFu;
+    mx = __vmaxu2(mx, m);
+    mn = __vminu2(mn, __vsub2(m, 0x00010001u));
+  }
+  const uint32_t bmax = max(mx & 0xFFFFu, mx >> 16);
+  const uint32_t bmin = min(mn & 0xFFFFu, mn >> 16) + 1u;  // 0x10000: all zero
+  if (bmax == 0u) return true;                               // all-zero chunk: y = 0
+  if (bmax >= 0x7F80u || bmin < 0x0080u) return false;      // inf/NaN or subnormal
+  constexpr int L2 = N0 == 4 ? 2 : 4;
+  return 1 + L2 + (int)((bmax >> 7) - (bmin >> 7)) + 8 <= 24;
+}
+
 // ---- out-of-line cold paths (kept out of the hot loop) ---------------------
 
 // Exact re-decision of flagged elements: bit (h*16 + e) of `m` flags
@@ -823,22 +871,28 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
              : static_cast<const void*>(reinterpret_cast<const char*>(a.x) + row * a.ldx * esz);
 
     // ---- pass 1: rotate, row absmax (NaN-propagating), best / 2nd pair ----
+    // best / second-best CHUNK maxima of this lane (bp = pair, bh = half)
     float lmax = 0.f, lmax_nan = 0.f, m2 = 0.f;
-    int bp = 0;
+    int bp = 0, bh = 0;
 #pragma unroll 1
     for (int p = 0; p < P; ++p) {
       float2 v[16];
       load_pair<F32, BULK, FULL>(v, rowp, ((int64_t)(2 * p) * W + w) * 32 + lane, cstride,
                                  nchunks);
       rotate_pair<N0>(v);
-      const float m = pair_absmax(v);
-      lmax_nan = max_nan(lmax_nan, m);
-      if (m > lmax) {
-        m2 = lmax;
-        lmax = m;
-        bp = p;
-      } else {
-        m2 = fmaxf(m2, m);
+      float mh[2];
+      pair_absmax2(v, mh[0], mh[1]);
+      lmax_nan = max_nan(lmax_nan, max_nan(mh[0], mh[1]));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (mh[h] > lmax) {
+          m2 = lmax;
+          lmax = mh[h];
+          bp = p;
+          bh = h;
+        } else {
+          m2 = fmaxf(m2, mh[h]);
+        }
       }
     }
     const float A32 = team_max_nan(lmax_nan, &ts, team, w, W);
@@ -860,7 +914,20 @@ __global__ void __launch_bounds__(kK1Threads, kK1MinBlocks) k1_rolled(K1Args a) 
         const bool all = m2 >= thr;
         double cmax = 0.0;
         if constexpr (N0 <= 16) {
-          if (has) {
+          bool settled = false;
+          if constexpr (!F32) {
+            // common case: every candidate lies in the lane's best chunk and
+            // that chunk passes the exponent-span certificate, so its y32 are
+            // exact and the candidates' exact maximum is lmax * rk (no
+            // re-rotation, no per-element settlement)
+            const int64_t bc = ((int64_t)(2 * bp + bh) * W + w) * 32 + lane;
+            if (has && !all && a.kind == kRotRegular && a.rot_cols >= a.K && bc < nchunks &&
+                chunk_certified_bf16<N0, BULK>(rowp, bc)) {
+              cmax = (double)lmax * rk;
+              settled = true;
+            }
+          }
+          if (has && !settled) {
 #pragma unroll 1
             for (int p = 0; p < P; ++p) {
               if (!(all || p == bp)) continue;

@@ -152,6 +152,52 @@ def test_k1_edge_rows():
         assert np.array_equal(s64.cpu().numpy(), sc)
 
 
+@pytest.mark.parametrize("K", [3072, 12288])
+@pytest.mark.parametrize("n0", [4, 16])
+def test_k1_row_max_settlement_paths(K, n0):
+    """The row-max settlement of the rolled kernel: the certified best-chunk
+    shortcut (companions within the exponent span), its fallbacks (span too
+    wide, subnormal companions, the max tied across chunks / lanes) and
+    wide-range rows, in packed and int8-code mode, bit-exact vs the oracle."""
+    rng = np.random.default_rng(K + n0)
+    M = 48
+    x = rng.standard_normal((M, K))
+    for r in range(M):
+        j = int(rng.integers(0, K // 16)) * 16
+        kind = r % 8
+        if kind == 0:    # spike, companions in span -> certified shortcut
+            x[r, j:j + 16] = 2.0 ** -2
+            x[r, j + 3] = 40.0
+        elif kind == 1:  # spike, companions far below -> span fails -> exact path
+            x[r, j:j + 16] = 2.0 ** -12
+            x[r, j + 5] = -40.0
+        elif kind == 2:  # subnormal-range companion in the spike's chunk
+            x[r, j + 1] = 1e-39
+            x[r, j + 7] = 50.0
+        elif kind == 3:  # the same spike in two chunks (candidates in both)
+            x[r, j + 2] = 45.0
+            x[r, (j + 16 * 37) % K + 2] = -45.0
+        elif kind == 4:  # wide dynamic range everywhere
+            x[r] *= 2.0 ** rng.integers(-20, 20, K)
+        elif kind == 5:  # zero chunk next to the maximum
+            x[r, j:j + 16] = 0.0
+            x[r, (j + 16) % K] = 60.0
+    xb = O.to_bf16_bits(x)
+    xt = bf16_tensor(xb)
+    xd = O.from_bf16_bits(xb)
+    spec = RotationSpec(RotationKind.regular, n0)
+    rot = O.group_rotate(xd, O.ROT_REGULAR, n0)
+    sc = O.compute_scales(rot)
+    q = O.quantize(rot, sc)
+    codes, s32, s64 = crt.rotate_quantize(xt, spec, QuantSpec(4), scales64=True)
+    assert np.array_equal(codes[:, :K // 2].cpu().numpy(), O.pack_int4_rows(q))
+    assert np.array_equal(s64.cpu().numpy(), sc)
+    c8, s8, sums = crt.rotate_quantize_i8(xt, spec)
+    assert np.array_equal(c8[:, :K].cpu().numpy().view(np.int8), q.astype(np.int8))
+    assert np.array_equal(s8.cpu().numpy(), sc.astype(np.float32))
+    assert np.array_equal(sums.cpu().numpy(), q.astype(np.int64).sum(1))
+
+
 def test_k1_nonfinite_raises_invalid_value():
     x = torch.randn(4, 256, device=DEV).to(torch.bfloat16)
     x[2, 17] = float("nan")
