@@ -230,18 +230,42 @@ struct V3Args {
   void* y;
   int64_t ldy;
   int32_t w8_ss;     // W8A8: A straight from shared memory (no TMEM copy)
+  int32_t y_tma;     // bf16 output through shared-memory staging + TMA bulk stores
 };
+
+// Epilogue output staging: one 32-token x 32-channel bf16 box (2 KB) per
+// epilogue warp, written with st.shared and stored by one TMA bulk tensor
+// store (the async proxy writes the 64 B rows; no per-lane global stores).
+constexpr int V3_YSTG = 2048;
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t saddr, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   map),
+               "r"(x), "r"(y), "r"(saddr)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // W8 = false: W4A4 (offset-binary int4 weights, hardware expansion);
 // W8 = true: W8A8 (int8 weights and activations).
 template <bool W8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     k3_v3_kernel(const __grid_constant__ CUtensorMap map_w,
-                 const __grid_constant__ CUtensorMap map_x, V3Args a) {
+                 const __grid_constant__ CUtensorMap map_x,
+                 const __grid_constant__ CUtensorMap map_y, V3Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = smem;                                        // V3_PS x (A 16 KB | B 12 KB)
   V3Smem* ss = reinterpret_cast<V3Smem*>(smem + V3_PS * V3_STAGE);
+  uint8_t* ystg = smem + V3_PS * V3_STAGE + ((sizeof(V3Smem) + 127) & ~(size_t)127);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -282,6 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
   if (warp == 0 && lane == 0) {  // kernel parameters, not predecessor output
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    if (a.y_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_y) : "memory");
   }
   griddep_launch();
   griddep_wait();
@@ -404,12 +429,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     const int h = (warp - 4) >> 2;
     const int et = threadIdx.x - 128;  // 0..255
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
+    const uint32_t ybuf = smem_u32(ystg) + (uint32_t)(warp - 4) * V3_YSTG;
     int ab = 0;
     uint32_t aph = 0;
     for (int t = pair; t < ntiles; t += npairs) {
       const int tt = t % a.ttiles, ct = t / a.ttiles;
       const int64_t mb = (int64_t)tt * V3_BT;                                // tile tokens
-      const int64_t n = (int64_t)ct * 2 * V3_BM + (int64_t)rank * V3_BM + q * 32 + lane;
+      const int64_t nw = (int64_t)ct * 2 * V3_BM + (int64_t)rank * V3_BM + q * 32;  // warp's channels
+      const int64_t n = nw + lane;
       const bool nok = n < a.N;
       const float sw = nok ? a.w_scales[n] : 0.f;
       const float bn = (a.bias && nok) ? a.bias[n] : 0.f;
@@ -426,6 +453,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         uint32_t acc[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32, acc);
         const int64_t m0 = mb + c * 32;  // tokens m0 .. m0+31 of this chunk
+        if (a.y_tma) {
+          // bf16 box via shared memory + one TMA store; the tensor map clips
+          // tokens >= M and channels >= N (their staged values are unused)
+          if (m0 >= a.M || nw >= a.N) continue;
+          uint32_t sav[32], smv[32];
+          lds_row32(smem_u32(&ss->sa[ab][c * 32]), sav);
+          if constexpr (!W8) lds_row32(smem_u32(&ss->sums[ab][c * 32]), smv);
+          if (lane == 0) bulk_wait_read0();  // the previous box has left the buffer
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
+            const __nv_bfloat16 o = __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
+            st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o));
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_y, ybuf, (int)nw, (int)m0);
+            bulk_commit();
+          }
+          continue;
+        }
         if (m0 >= a.M || !nok) continue;
         const int jn = a.M - m0 < 32 ? (int)(a.M - m0) : 32;
         const int* sm = &ss->sums[ab][c * 32];
@@ -470,6 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         aph ^= 1;
       }
     }
+    if (a.y_tma && lane == 0) bulk_wait0();  // every box written before the CTA exits
   }
 
   tc_fence_before();
@@ -544,7 +595,25 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  // bf16 output map: N channels (inner) x M tokens, 32 x 32 boxes
+  CUtensorMap my = mx;
+  static const bool direct_stores = [] {  // A/B switch: the per-lane direct stores
+    const char* e = getenv("CRT_K3_DIRECT_STORES");
+    return e && e[0] == '1';
+  }();
+  bool y_tma = false;
+  if (a.out_kind == 0 && !direct_stores && (uintptr_t)a.y % 16 == 0 && (a.ldy * 2) % 16 == 0) {
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)(a.ldy * 2)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    y_tma = fn(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.y, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (!y_tma) my = mx;
+  }
   V3Args v{};
+  v.y_tma = y_tma ? 1 : 0;
   v.M = a.M;
   v.N = a.N;
   v.K = a.K;
@@ -562,7 +631,8 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
     return e && e[0] == '1';
   }();
   v.w8_ss = w8 && !w8_ts;
-  const size_t smem = 1024 + V3_PS * V3_STAGE + sizeof(V3Smem);
+  const size_t smem =
+      1024 + V3_PS * V3_STAGE + ((sizeof(V3Smem) + 127) & ~(size_t)127) + 8 * V3_YSTG;
   auto kern = w8 ? k3_v3_kernel<true> : k3_v3_kernel<false>;
   static SmemAttr attr[2];
   {
@@ -573,7 +643,7 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
   const cudaError_t le = launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(V3_THREADS), smem, st,
-                                    mw, mx, v);
+                                    mw, mx, my, v);
   ++*launches;
   return le;
 }
