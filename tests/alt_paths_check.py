@@ -1,6 +1,6 @@
 """Parity of the opt-in kernel paths, run in a subprocess by
 tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K1_FAST=1 / CRT_K3_V1=1 /
-CRT_K3_W8_TS=1 set before the library loads (the switches are read once per
+CRT_K3_W8_TS=1 / CRT_K3_DIRECT_STORES=1 (or nothing: the default paths) set before the library loads (the switches are read once per
 process).  W4A4 against the oracle; W8A8 accumulators against the exact
 integer GEMM of the exported codes."""
 import sys
@@ -34,6 +34,10 @@ def main():
                                       O.pack_int4_rows(f["act_codes"])), (n0, fam, m, k)
                 assert np.array_equal(s64.cpu().numpy(), f["act_scales"]), (n0, fam, m, k)
                 assert np.array_equal(acc.cpu().numpy(), f["acc"]), (n0, fam, m, k)
+                # bf16 output (ragged token / channel boxes) vs the f32 output
+                y16 = crt.forward(x, layer, QuantSpec(4), out="bf16").float().cpu().numpy()
+                y32 = crt.forward(x, layer, QuantSpec(4), out="f32").cpu().numpy()
+                assert (np.abs(y16 - y32) <= 2.0 ** -8 * np.abs(y32) + 1e-30).all(), (n0, fam, m, k)
     # W8A8 (f1): the v3 SS / TMEM-copy / v1 GEMMs against the exact integer GEMM
     q8 = QuantSpec(8)
     for (m, k, n) in ((97, 3072, 300), (193, 12288, 256)):

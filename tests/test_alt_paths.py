@@ -1,6 +1,7 @@
 """Opt-in kernel paths stay bit-exact: the tensor-core K1 (CRT_K1_MMA=1), the
 register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
-(CRT_K3_V1=1) and the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1), each in a fresh
+(CRT_K3_V1=1), the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-lane
+store epilogue (CRT_K3_DIRECT_STORES=1), each -- and the defaults -- in a fresh
 process."""
 import os
 import subprocess
@@ -12,8 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K3_V1": "1"},
-                                 {"CRT_K3_W8_TS": "1"}])
+@pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K3_V1": "1"},
+                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_DIRECT_STORES": "1"}])
 def test_opt_in_paths_bit_exact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
