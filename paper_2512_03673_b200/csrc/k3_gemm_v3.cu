@@ -230,6 +230,7 @@ struct V3Args {
   void* y;
   int64_t ldy;
   int32_t w8_ss;     // W8A8: A straight from shared memory (no TMEM copy)
+  int32_t fdq;       // magic-number fp32x2 dequant in the TMA-store epilogue
   int32_t y_tma;     // bf16 output through shared-memory staging + TMA bulk stores
 };
 
@@ -430,6 +431,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     const int et = threadIdx.x - 128;  // 0..255
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
     const uint32_t ybuf = smem_u32(ystg) + (uint32_t)(warp - 4) * V3_YSTG;
+    // fdq: integer-to-float by the magic constant, two tokens per fp32x2
+    // instruction; exact while |4*sum(w*a)| < 2^22 (4*49*K < 2^22: K <= 21384)
+    const bool fdq = !W8 && a.y_tma && a.fdq && a.K <= 21384;
     int ab = 0;
     uint32_t aph = 0;
     for (int t = pair; t < ntiles; t += npairs) {
@@ -443,7 +447,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
       for (int i = et; i < V3_BT; i += 256) {
         const int64_t m = mb + i;
         ss->sa[ab][i] = m < a.M ? a.a_scales[m] : 0.f;
-        ss->sums[ab][i] = (W8 || m >= a.M) ? 0 : 32 * a.a_sums[m];
+        const int off = (W8 || m >= a.M) ? 0 : 32 * a.a_sums[m];
+        // magic-number dequant (fdq): acc' + (0x4B400000 - 32 S_a) are the
+        // float bits of 1.5*2^23 + 4*sum(w*a)
+        ss->sums[ab][i] = fdq ? (int)(0x4B400000u - (uint32_t)off) : off;
       }
       named_bar_sync(1, 256);
       wait_sleep(&ss->acc_full[ab], aph);
@@ -462,11 +469,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
           if constexpr (!W8) lds_row32(smem_u32(&ss->sums[ab][c * 32]), smv);
           if (lane == 0) bulk_wait_read0();  // the previous box has left the buffer
           __syncwarp();
+          if (fdq) {
+            // v = (acc' - 32 S_a) / 4 exactly: fma(1.5*2^23 + 4v, 1/4, -1.5*2^21);
+            // then the same fp32 expression as below, two tokens at a time
+            const float2 q4 = make_float2(0.25f, 0.25f), mc = make_float2(-3145728.f, -3145728.f);
+            const float2 w2 = make_float2(sw, sw), b2 = make_float2(bn, bn);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
-            const __nv_bfloat16 o = __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
-            st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o));
+            for (int j = 0; j < 32; j += 2) {
+              const float2 mm = make_float2(__uint_as_float(acc[j] + smv[j]),
+                                            __uint_as_float(acc[j + 1] + smv[j + 1]));
+              const float2 v = __ffma2_rn(mm, q4, mc);
+              const float2 p =
+                  __fmul2_rn(v, make_float2(__uint_as_float(sav[j]), __uint_as_float(sav[j + 1])));
+              const __nv_bfloat162 o = __float22bfloat162_rn(__ffma2_rn(p, w2, b2));
+              st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o.x));
+              st_shared_u16(ybuf + (uint32_t)(j + 1) * 64u + (uint32_t)lane * 2u,
+                            __bfloat16_as_ushort(o.y));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
+              const __nv_bfloat16 o =
+                  __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
+              st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o));
+            }
           }
           fence_proxy_async();
           __syncwarp();
@@ -614,6 +641,11 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   }
   V3Args v{};
   v.y_tma = y_tma ? 1 : 0;
+  static const bool no_fdq = [] {  // A/B switch: per-token I2F dequant
+    const char* e = getenv("CRT_K3_NO_FDQ");
+    return e && e[0] == '1';
+  }();
+  v.fdq = no_fdq ? 0 : 1;
   v.M = a.M;
   v.N = a.N;
   v.K = a.K;

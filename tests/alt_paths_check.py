@@ -3,6 +3,7 @@ tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K1_FAST=1 / CRT_K3_V1=1 /
 CRT_K3_W8_TS=1 / CRT_K3_DIRECT_STORES=1 (or nothing: the default paths) set before the library loads (the switches are read once per
 process).  W4A4 against the oracle; W8A8 accumulators against the exact
 integer GEMM of the exported codes."""
+import hashlib
 import sys
 
 import numpy as np
@@ -17,6 +18,7 @@ from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec  # noqa:
 def main():
     dev = "cuda"
     to_t = lambda b: torch.from_numpy(b.astype(np.uint16).view(np.int16)).to(dev).view(torch.bfloat16)  # noqa: E731
+    y16_hash = hashlib.md5()
     for n0 in (4, 16):
         for fam in ("gaussian", "colwise", "rowwise"):
             for (m, k, n) in ((97, 3072, 80), (40, 12288, 48)):
@@ -35,7 +37,9 @@ def main():
                 assert np.array_equal(s64.cpu().numpy(), f["act_scales"]), (n0, fam, m, k)
                 assert np.array_equal(acc.cpu().numpy(), f["acc"]), (n0, fam, m, k)
                 # bf16 output (ragged token / channel boxes) vs the f32 output
-                y16 = crt.forward(x, layer, QuantSpec(4), out="bf16").float().cpu().numpy()
+                y16t = crt.forward(x, layer, QuantSpec(4), out="bf16")
+                y16_hash.update(y16t.view(torch.int16).cpu().numpy().tobytes())
+                y16 = y16t.float().cpu().numpy()
                 y32 = crt.forward(x, layer, QuantSpec(4), out="f32").cpu().numpy()
                 assert (np.abs(y16 - y32) <= 2.0 ** -8 * np.abs(y32) + 1e-30).all(), (n0, fam, m, k)
     # W8A8 (f1): the v3 SS / TMEM-copy / v1 GEMMs against the exact integer GEMM
@@ -51,6 +55,7 @@ def main():
         ref = (a8 @ b8.T).round().to(torch.int64)
         got = crt.forward(x, layer, q8, out="i32").to(torch.int64)
         assert torch.equal(got, ref), ("w8a8", m, k, n)
+    print("bf16 outputs md5", y16_hash.hexdigest())
     print("ok")
 
 

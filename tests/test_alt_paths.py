@@ -14,9 +14,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K3_V1": "1"},
-                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_DIRECT_STORES": "1"}])
+                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_DIRECT_STORES": "1"},
+                                 {"CRT_K3_NO_FDQ": "1"}])
 def test_opt_in_paths_bit_exact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_epilogue_variants_bit_identical_bf16():
+    """The TMA-store epilogue with the magic-number dequant (default), with
+    the per-token I2F dequant (CRT_K3_NO_FDQ=1) and the per-lane direct
+    stores (CRT_K3_DIRECT_STORES=1) write the same bf16 bits."""
+    digests = []
+    for env in ({}, {"CRT_K3_NO_FDQ": "1"}, {"CRT_K3_DIRECT_STORES": "1"}):
+        e = dict(os.environ, **env)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
+                           cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        digests.append([l for l in r.stdout.splitlines() if l.startswith("bf16 outputs md5")][0])
+    assert len(set(digests)) == 1, digests
