@@ -262,6 +262,12 @@ const char* crt_last_error(void);
 crt_status crt_device_status(void* stream, int32_t reset);
 /* Number of CUDA kernels this library has launched (process lifetime). */
 int64_t crt_launch_count(void);
+
+/* Dev aid (not part of the reference surface): when buf is non-null, the
+ * K1 team kernel records %globaltimer stamps into it, 26 uint64 words per
+ * CTA (kernel start, after the PDL wait, then per row: data ready, team
+ * barrier passed, row done, for the first 8 rows).  NULL turns it off. */
+void crt_debug_k1_trace(void* buf);
 int32_t crt_abi_version(void);
 
 #ifdef __cplusplus

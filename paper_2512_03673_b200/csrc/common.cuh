@@ -17,6 +17,12 @@ enum : int { kRotNone = 0, kRotSylvester = 1, kRotRegular = 2 };
 // compute_scales (quant.cpp:16-18).
 __device__ __forceinline__ void flag_invalid_value(int* err) { atomicOr(err, 1); }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---- packed fp32x2 arithmetic (FADD2 / FFMA2 on sm_100) -------------------
 __device__ __forceinline__ uint64_t f2_bits(float2 a) {
   uint64_t r;

@@ -1534,6 +1534,7 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
 
 }  // namespace crt
 #include "k1_mma.cuh"
+#include "k1_team.cuh"
 namespace crt {
 
 template <int N0, bool F32, int BITS>
@@ -1550,6 +1551,7 @@ cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
       if (e != cudaErrorInvalidValue) return e;
     }
   }
+  if (k1_team_ok(a, F32, BITS)) return launch_team<N0, F32, BITS>(a, st, l);
   static const bool fast = [] {
     const char* e = getenv("CRT_K1_FAST");
     return e && e[0] == '1';

@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "k1_rotate_quant.h"
 #include <stdio.h>
+#include <atomic>
 
 namespace crt {
 
@@ -13,6 +14,12 @@ template <bool F32, int BITS>
 cudaError_t k1_dispatch(const K1Args& a, int n0, cudaStream_t st, int64_t* l);
 template <bool F32, int BITS>
 cudaError_t k1_exact_launch(const K1Args& a, cudaStream_t st);
+
+namespace {
+std::atomic<unsigned long long*> g_trace{nullptr};
+}
+void set_k1_trace(unsigned long long* buf) { g_trace.store(buf); }
+unsigned long long* k1_trace() { return g_trace.load(); }
 
 // ---------------------------------------------------------------------------
 // Host launcher
@@ -74,6 +81,7 @@ cudaError_t launch_k1(const K1Args& a, const K1Plan& p, bool f32, int bits, cuda
                       int64_t* launches) {
   if (p.fast) {
     K1Args b = a;
+    b.trace = k1_trace();
     b.team_warps = p.W;
     b.chunks = p.C;
     const int n0 = a.kind == kRotNone ? 1 : (int)a.group;

@@ -26,7 +26,13 @@ struct K1Args {
   const double* amax_in;  // nullable: use this exact per-row max |y_ref| for the scale
                           // (row-parallel: the MAX all-reduce of the shards' maxima)
   int* err;           // device error word
+  unsigned long long* trace;  // nullable dev aid: per-CTA globaltimer stamps (k1_team)
 };
+
+// Dev aid (crt_debug_k1_trace): when set, k1_team records globaltimer
+// stamps per CTA into this device buffer (kK1TraceWords words per CTA).
+void set_k1_trace(unsigned long long* buf);
+unsigned long long* k1_trace();
 
 struct K1Plan {
   bool fast;
