@@ -39,12 +39,13 @@ q = lambda a: "p10 %6.2f  p50 %6.2f  p90 %6.2f  max %6.2f" % tuple(  # noqa: E73
 print(f"M={M} K={K} N0={n0}: {len(t)} CTAs, end {np.nanmax(t):.2f} us after the first start")
 print("start        ", q(t[:, 0]))
 print("pdl wait done", q(t[:, 1]))
-# per row i: [2+3i] data ready (P1 start), [3+3i] thread 0 finished P2,
-# [4+3i] the row's last warp finished the bookkeeping (may be absent)
+# per row i (thread 0): [2+3i] data ready, [3+3i] team barrier passed,
+# [4+3i] row done
 for i in range(ROWS):
     r = t[:, 2 + 3 * i: 5 + 3 * i]
     if np.all(np.isnan(r[:, 0])):
         break
-    print(f"row {i}: ready   ", q(r[:, 0]))
-    print(f"       P2 done ", q(r[:, 1] - r[:, 0]), "(after ready)")
-    print(f"       booked  ", q(r[:, 2]))
+    print(f"row {i}: ready  ", q(r[:, 0]))
+    print(f"       barrier", q(r[:, 1] - r[:, 0]), "(after ready)")
+    print(f"       done   ", q(r[:, 2] - r[:, 1]), "(after barrier)")
+    print(f"       end    ", q(r[:, 2]))
