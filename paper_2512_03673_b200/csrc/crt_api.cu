@@ -147,8 +147,9 @@ struct crt_layer {
   crt_layer_desc desc;
   int64_t n_total;      // N of the full layer (== desc.out_features unless sharded)
   int64_t row_offset;   // first output channel of this shard
-  uint8_t* codes;       // N x ldc, reference row layout (packed int4 / int8)
-  int64_t ldc;
+  uint8_t* codes;       // bits 8: N x ldc int8 codes (K3's operand); bits 4: null --
+                        // the only copy is tiles' offset-binary one
+  int64_t ldc;          // reference-layout row pitch (scratch / export layout)
   float* s32;           // N
   double* s64;          // N
   float* bias;          // N or null
@@ -284,7 +285,12 @@ static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t l
   L->ldc = d->bits_w == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
   cudaError_t e = cudaSuccess;
   size_t nalloc = (size_t)(Ns ? Ns : 1);
-  if (e == cudaSuccess) e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  // bits 4: K1 writes the reference layout into a stream-ordered scratch
+  // buffer; the layer keeps only K3's offset-binary copy (one copy of the
+  // weights, like the reference PreparedLayer, pipeline.hpp:55-65)
+  uint8_t* wcodes = nullptr;
+  if (d->bits_w == 4) e = cudaMallocAsync(reinterpret_cast<void**>(&wcodes), (size_t)L->ldc * nalloc, st);
+  else e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc), wcodes = L->codes;
   if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
   if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
   if (e == cudaSuccess && bias) {
@@ -292,21 +298,28 @@ static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t l
     if (e == cudaSuccess && Ns)
       e = cudaMemcpyAsync(L->bias, bias + off, 4 * Ns, cudaMemcpyDeviceToDevice, st);
   }
+  auto drop_scratch = [&]() {
+    if (d->bits_w == 4 && wcodes) cudaFreeAsync(wcodes, st);
+    wcodes = nullptr;
+  };
   if (e != cudaSuccess) {
+    drop_scratch();
     crt_layer_destroy(L);
     return cuda_fail(e, "layer alloc");
   }
   // K1 on the weight rows: rotation along K, per-output-channel scales.
   const char* wbase = reinterpret_cast<const char*>(w) + off * ldw * esz;
-  crt_status s = run_k1(wbase, d->w_dtype, Ns, K, ldw, &d->rotation, d->bits_w, L->codes, L->ldc,
+  crt_status s = run_k1(wbase, d->w_dtype, Ns, K, ldw, &d->rotation, d->bits_w, wcodes, L->ldc,
                         L->s32, L->s64, st);
   if (s != CRT_OK) {
+    drop_scratch();
     crt_layer_destroy(L);
     return s;
   }
   int64_t launches = 0;
-  e = crt::k3_prepare_weights(L->codes, L->ldc, Ns, K, d->bits_w, &L->tiles, st, &launches);
+  e = crt::k3_prepare_weights(wcodes, L->ldc, Ns, K, d->bits_w, &L->tiles, st, &launches);
   g_launches += launches;
+  drop_scratch();
   if (e != cudaSuccess) {
     crt_layer_destroy(L);
     return cuda_fail(e, "weight tiling");
@@ -348,25 +361,34 @@ crt_status crt_layer_from_codes(const crt_layer_desc* d, const uint8_t* codes_ho
     s64[n] = (double)scales_host[n];
     if (bias_host) b32[n] = (float)bias_host[n];
   }
-  cudaError_t e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  // bits 4: the host codes are staged in a scratch buffer and kept only as
+  // K3's offset-binary copy
+  uint8_t* wcodes = nullptr;
+  cudaError_t e = cudaMalloc(&wcodes, (size_t)L->ldc * nalloc);
+  if (d->bits_w == 8) L->codes = wcodes;
   if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
   if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
   if (e == cudaSuccess && bias_host) e = cudaMalloc(&L->bias, 4 * nalloc);
-  if (e == cudaSuccess) e = cudaMemsetAsync(L->codes, 0, (size_t)L->ldc * nalloc, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(wcodes, 0, (size_t)L->ldc * nalloc, st);
   if (e == cudaSuccess && N && row)
-    e = cudaMemcpy2DAsync(L->codes, L->ldc, codes_host, ld_codes, row, N, cudaMemcpyHostToDevice, st);
+    e = cudaMemcpy2DAsync(wcodes, L->ldc, codes_host, ld_codes, row, N, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s32, scales_host, 4 * N, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s64, s64.data(), 8 * N, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && bias_host && N)
     e = cudaMemcpyAsync(L->bias, b32.data(), 4 * N, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host staging vectors go out of scope
   if (e != cudaSuccess) {
+    if (d->bits_w == 4) cudaFree(wcodes);
     crt_layer_destroy(L);
     return cuda_fail(e, "layer_from_codes");
   }
   int64_t launches = 0;
-  e = crt::k3_prepare_weights(L->codes, L->ldc, N, K, d->bits_w, &L->tiles, st, &launches);
+  e = crt::k3_prepare_weights(wcodes, L->ldc, N, K, d->bits_w, &L->tiles, st, &launches);
   g_launches += launches;
+  if (d->bits_w == 4) {
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(wcodes);
+  }
   if (e != cudaSuccess) {
     crt_layer_destroy(L);
     return cuda_fail(e, "weight tiling");
@@ -422,27 +444,33 @@ crt_status crt_layer_prepare_kshard(const crt_layer_desc* d, const void* w, int6
   const int64_t row = d->bits_w == 4 ? Ks / 2 : Ks;
   L->ldc = (row + 15) / 16 * 16;
   const size_t nalloc = (size_t)(N ? N : 1);
-  cudaError_t e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+  cudaError_t e = cudaSuccess;
+  if (d->bits_w == 8) {
+    e = cudaMalloc(&L->codes, (size_t)L->ldc * nalloc);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L->codes, 0, (size_t)L->ldc * nalloc, st);
+    if (e == cudaSuccess && N && row)
+      e = cudaMemcpy2DAsync(L->codes, L->ldc, full->codes + (int64_t)rank * row, full->ldc, row, N,
+                            cudaMemcpyDeviceToDevice, st);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&L->s32, 4 * nalloc);
   if (e == cudaSuccess) e = cudaMalloc(&L->s64, 8 * nalloc);
   if (e == cudaSuccess && bias) e = cudaMalloc(&L->bias, 4 * nalloc);
-  if (e == cudaSuccess) e = cudaMemsetAsync(L->codes, 0, (size_t)L->ldc * nalloc, st);
-  if (e == cudaSuccess && N && row)
-    e = cudaMemcpy2DAsync(L->codes, L->ldc, full->codes + (int64_t)rank * row, full->ldc, row, N,
-                          cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s32, full->s32, 4 * N, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess && N) e = cudaMemcpyAsync(L->s64, full->s64, 8 * N, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess && bias && N)
     e = cudaMemcpyAsync(L->bias, full->bias, 4 * N, cudaMemcpyDeviceToDevice, st);
+  int64_t launches = 0;
+  if (e == cudaSuccess) {
+    // bits 4: the shard's columns straight from the full layer's
+    // offset-binary copy (byte offset rank * Ks/2 of every row)
+    e = d->bits_w == 4
+            ? crt::k3_prepare_weights(full->tiles.codes_ob + (int64_t)rank * row, full->tiles.ld_ob,
+                                      N, Ks, 4, &L->tiles, st, &launches, /*src_ob=*/true)
+            : crt::k3_prepare_weights(L->codes, L->ldc, N, Ks, 8, &L->tiles, st, &launches);
+  }
+  g_launches += launches;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   crt_layer_destroy(full);
-  if (e != cudaSuccess) {
-    crt_layer_destroy(L);
-    return cuda_fail(e, "kshard copy");
-  }
-  int64_t launches = 0;
-  e = crt::k3_prepare_weights(L->codes, L->ldc, N, Ks, d->bits_w, &L->tiles, st, &launches);
-  g_launches += launches;
   if (e != cudaSuccess) {
     crt_layer_destroy(L);
     return cuda_fail(e, "weight tiling");
@@ -477,7 +505,13 @@ crt_status crt_layer_export(const crt_layer* L, uint8_t* codes, int64_t ld_codes
   cudaError_t e = cudaSuccess;
   if (codes && N && row) {
     if (ld_codes < row) return fail(CRT_ERR_SHAPE, "ld_codes too small");
-    e = cudaMemcpy2DAsync(codes, ld_codes, L->codes, L->ldc, row, N, cudaMemcpyDeviceToDevice, st);
+    if (L->desc.bits_w == 4) {  // back from the offset-binary copy
+      int64_t launches = 0;
+      e = crt::k3_export_w4(L->tiles, codes, ld_codes, 0, row, st, &launches);
+      g_launches += launches;
+    } else {
+      e = cudaMemcpy2DAsync(codes, ld_codes, L->codes, L->ldc, row, N, cudaMemcpyDeviceToDevice, st);
+    }
   }
   if (e == cudaSuccess && s32 && N) e = cudaMemcpyAsync(s32, L->s32, 4 * N, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess && s64 && N) e = cudaMemcpyAsync(s64, L->s64, 8 * N, cudaMemcpyDeviceToDevice, st);

@@ -222,6 +222,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1) k3_ss_kernel(K3Args a) {
             const int64_t n = n0 + r;
             if (n < a.N && kbyte < kbytes)
               v[q] = __ldg(reinterpret_cast<const uint4*>(wcodes + n * ldw + kbyte));
+            if (BITS == 4 && a.w.ob) {  // offset-binary weights -> two's complement
+              v[q].x ^= 0x88888888u;
+              v[q].y ^= 0x88888888u;
+              v[q].z ^= 0x88888888u;
+              v[q].w ^= 0x88888888u;
+            }
           }
         }
         if (b0 == 0) mbar_wait(&ss->empty[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
@@ -328,7 +334,12 @@ __global__ void k3_generic_kernel(K3Args a) {
   const uint8_t* ar = a.a_codes + m * a.lda;
   const uint8_t* wr = a.w.codes + n * a.w.ld;
   int32_t acc = 0;
-  for (int64_t k = 0; k < a.K; ++k) acc += code_at<BITS>(ar, k) * code_at<BITS>(wr, k);
+  const int wflip = BITS == 4 && a.w.ob ? 8 : 0;  // offset-binary weight nibbles
+  for (int64_t k = 0; k < a.K; ++k) {
+    int wc = code_at<BITS>(wr, k);
+    if (wflip) wc = ((wc & 15) ^ 8) - 8;  // nibble n -> (n ^ 8) as two's complement
+    acc += code_at<BITS>(ar, k) * wc;
+  }
   if (a.out_kind == 2) {
     reinterpret_cast<int32_t*>(a.y)[m * a.ldy + n] = acc;
   } else {
@@ -341,17 +352,29 @@ __global__ void k3_generic_kernel(K3Args a) {
 }  // namespace
 
 __global__ void k3_offset_binary_kernel(const uint8_t* src, int64_t lds, int64_t row_bytes,
-                                        uint8_t* dst, int64_t ldd, int64_t n) {
-  // two's-complement nibble <-> offset binary: flip bit 3; pad = code 0
+                                        uint8_t* dst, int64_t ldd, int64_t n, uint8_t flip) {
+  // two's-complement nibble -> offset binary: flip bit 3 (flip = 0x88; 0 if
+  // the source is offset binary already); pad = code 0 (0x8)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / ldd, c = i - r * ldd;
-    dst[i] = c < row_bytes ? src[r * lds + c] ^ 0x88 : 0x88;
+    dst[i] = c < row_bytes ? src[r * lds + c] ^ flip : 0x88;
+  }
+}
+
+__global__ void k3_xor_copy_kernel(const uint8_t* src, int64_t lds, uint8_t* dst, int64_t ldd,
+                                   int64_t row_bytes, int64_t n) {
+  // dst row r = src row r with every nibble's bit 3 flipped (offset binary <->
+  // two's complement), row_bytes per row
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / row_bytes, c = i - r * row_bytes;
+    dst[r * ldd + c] = src[r * lds + c] ^ 0x88;
   }
 }
 
 cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int64_t K, int bits,
-                               K3Weights* out, cudaStream_t st, int64_t* launches) {
+                               K3Weights* out, cudaStream_t st, int64_t* launches, bool src_ob) {
   out->codes = codes;
   out->codes_ob = nullptr;
   out->ld_ob = 0;
@@ -359,18 +382,35 @@ cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int
   out->N = N;
   out->K = K;
   out->bits = bits;
-  if (bits != 4 || N == 0) return cudaSuccess;
-  // v3 operand: offset-binary copy (TMA 16U4 + tcgen05.cp decompress -> 4*(w+8))
+  out->ob = 0;
+  if (bits != 4) return cudaSuccess;
+  // the single 4-bit copy: offset binary (TMA 16U4 + tcgen05.cp decompress
+  // -> 4*(w+8) for v3; v1 / v2 flip it back as they expand)
   uint8_t* ob = nullptr;
   const int64_t ldo = (K + 127) / 128 * 64;
-  cudaError_t e = cudaMalloc(&ob, (size_t)ldo * N);
+  cudaError_t e = cudaMalloc(&ob, (size_t)ldo * (N ? N : 1));
   if (e != cudaSuccess) return e;
   const int64_t n = ldo * N;
-  k3_offset_binary_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(
-      codes, ldc, (K + 1) / 2, ob, ldo, n);
-  out->ld_ob = ldo;
-  ++*launches;
+  if (n > 0) {
+    k3_offset_binary_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0,
+                              st>>>(codes, ldc, (K + 1) / 2, ob, ldo, n, src_ob ? 0x00 : 0x88);
+    ++*launches;
+  }
+  out->codes = ob;
   out->codes_ob = ob;
+  out->ld_ob = ldo;
+  out->ld = ldo;
+  out->ob = 1;
+  return cudaGetLastError();
+}
+
+cudaError_t k3_export_w4(const K3Weights& w, uint8_t* dst, int64_t ldd, int64_t col_byte0,
+                         int64_t row_bytes, cudaStream_t st, int64_t* launches) {
+  const int64_t n = row_bytes * w.N;
+  if (n <= 0) return cudaSuccess;
+  k3_xor_copy_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(
+      w.codes_ob + col_byte0, w.ld_ob, dst, ldd, row_bytes, n);
+  ++*launches;
   return cudaGetLastError();
 }
 

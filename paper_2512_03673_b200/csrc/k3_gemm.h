@@ -6,18 +6,24 @@
 
 namespace crt {
 
-// Prepared weight operand.  Codes are row-major per output channel (n), in
-// the reference pack_int4 nibble order (bits 4) or int8 (bits 8), with a
-// 16-byte aligned row pitch `ld` so every 32-code K-chunk is one aligned
+// Prepared weight operand.  Codes are row-major per output channel (n) with
+// a 16-byte aligned row pitch `ld`, so every 32-code K-chunk is one aligned
 // 16-byte vector (the unit K3 stages).
+//  * bits 8: int8 codes (the layer's own buffer).
+//  * bits 4: ONE copy, owned here, in offset binary (nibble = code + 8, the
+//    pack_int4 nibble order, K padded to 128 codes with code 0 = 0x8):
+//    codes == codes_ob, ob = 1.  v3 feeds it to TMA 16U4 + tcgen05.cp
+//    decompression as is; v1 / v2 / the generic kernel flip bit 3 of every
+//    nibble (XOR 0x88) as they expand, and export converts on the way out.
 struct K3Weights {
   const uint8_t* codes;
-  const uint8_t* codes_ob;  // same codes in offset binary (nibble = code + 8), v3 / owned
+  const uint8_t* codes_ob;  // bits 4: the offset-binary codes (== codes); else null
   int64_t ld_ob;            // its row pitch: K rounded up to 128 codes (64 B; TMA 16U4 needs it)
   int64_t ld;
   int64_t N;
   int64_t K;
   int32_t bits;
+  int32_t ob;               // codes are offset binary (bits 4)
 };
 
 struct K3Args {
@@ -36,8 +42,17 @@ struct K3Args {
   int64_t ldy;
 };
 
+// bits 4: builds the owned offset-binary copy from `codes` (reference
+// pack_int4 layout, row pitch ldc; or already offset binary when src_ob);
+// the caller may free `codes` afterwards (stream-ordered).  bits 8: refers
+// to `codes`, which must outlive the weights.
 cudaError_t k3_prepare_weights(const uint8_t* codes, int64_t ldc, int64_t N, int64_t K, int bits,
-                               K3Weights* out, cudaStream_t st, int64_t* launches);
+                               K3Weights* out, cudaStream_t st, int64_t* launches,
+                               bool src_ob = false);
+// Reference-layout copy of prepared 4-bit weights (XOR 0x88 back to two's
+// complement): row r of dst gets (K + 1) / 2 bytes.
+cudaError_t k3_export_w4(const K3Weights& w, uint8_t* dst, int64_t ldd, int64_t col_byte0,
+                         int64_t row_bytes, cudaStream_t st, int64_t* launches);
 void k3_free_weights(K3Weights* w);
 cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 

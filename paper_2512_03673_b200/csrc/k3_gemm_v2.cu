@@ -225,6 +225,7 @@ struct V2Args {
   int32_t out_kind;  // 0 bf16, 1 f32, 2 int32 accumulators
   void* y;
   int64_t ldy;
+  int32_t w_ob;      // weights in offset binary (flip bit 3 of each nibble)
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
@@ -383,6 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
     // MMA K-block periods to cover its load -> expand -> store -> fence chain.
     const int grp = (warp - 8) >> 2;
     const int e = threadIdx.x - 256 - grp * 128;  // 0..127
+    const uint32_t wflip = a.w_ob ? 0x80808080u : 0u;
     const uint32_t full_st = mapa(smem_u32(&ss->st_full[0]), 0);
     int c = 0;  // global K-block counter of this CTA
     for (int t = pair; t < ntiles; t += npairs) {
@@ -412,14 +414,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS, 1)
           const int r = u >> 2, j = u & 3;
           const uint4 v = p[i];
           uint4 c0, c1;
-          c0.x = (v.x << 4) & 0xF0F0F0F0u;
-          c0.y = v.x & 0xF0F0F0F0u;
-          c0.z = (v.y << 4) & 0xF0F0F0F0u;
-          c0.w = v.y & 0xF0F0F0F0u;
-          c1.x = (v.z << 4) & 0xF0F0F0F0u;
-          c1.y = v.z & 0xF0F0F0F0u;
-          c1.z = (v.w << 4) & 0xF0F0F0F0u;
-          c1.w = v.w & 0xF0F0F0F0u;
+          // offset-binary weights: flipping bit 7 of each code*16 byte is
+          // the nibble's bit 3 (one LOP3 with the mask)
+          c0.x = ((v.x << 4) & 0xF0F0F0F0u) ^ wflip;
+          c0.y = (v.x & 0xF0F0F0F0u) ^ wflip;
+          c0.z = ((v.y << 4) & 0xF0F0F0F0u) ^ wflip;
+          c0.w = (v.y & 0xF0F0F0F0u) ^ wflip;
+          c1.x = ((v.z << 4) & 0xF0F0F0F0u) ^ wflip;
+          c1.y = (v.z & 0xF0F0F0F0u) ^ wflip;
+          c1.z = ((v.w << 4) & 0xF0F0F0F0u) ^ wflip;
+          c1.w = (v.w & 0xF0F0F0F0u) ^ wflip;
           uint8_t* rowp = tile + r * 128;
           const int s7 = r & 7;
           *reinterpret_cast<uint4*>(rowp + (((2 * j) ^ s7) << 4)) = c0;
@@ -580,6 +584,7 @@ cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.out_kind = a.out_kind;
   v.y = a.y;
   v.ldy = a.ldy;
+  v.w_ob = a.w.ob;
   const size_t smem = 1024 + V2_PS * V2_PK_STAGE + V2_KS * V2_B8_STAGE + sizeof(V2Smem);
   static SmemAttr attr;
   {

@@ -95,6 +95,11 @@ class FluxStack:
             groups.setdefault(l.group if fused else l.name, []).append(l)
         self.units: List[Tuple[List[Linear], api.PreparedLayer]] = []
         g = torch.Generator(device=self.device)
+        # device memory the prepared layers own (cudaMalloc'd by the library,
+        # outside torch's caching allocator): free-memory drop minus torch's
+        # own reserve growth (the random bf16 weights are torch tensors)
+        torch.cuda.synchronize(self.device)
+        free0, res0 = torch.cuda.mem_get_info(self.device)[0], torch.cuda.memory_reserved(self.device)
         for i, (key, ls) in enumerate(groups.items()):
             ws, bs = [], []
             for l in ls:
@@ -106,6 +111,9 @@ class FluxStack:
             b = torch.cat(bs, 0) if len(bs) > 1 else bs[0]
             self.units.append((ls, api.prepare_layer(w, b, self.spec, self.q, key)))
             del w, ws
+        torch.cuda.synchronize(self.device)
+        self.layer_bytes = ((free0 - torch.cuda.mem_get_info(self.device)[0])
+                            - (torch.cuda.memory_reserved(self.device) - res0))
         # one synthetic input per (M, K) shape, reused by every linear of that shape
         self.inputs: Dict[Tuple[int, int], torch.Tensor] = {}
         for ls, _ in self.units:

@@ -37,7 +37,8 @@ for fused, streams in ((False, 1), (True, 1), (True, 2)):
                       "fused_siblings": fused, "cuda_streams": streams,
                       "units": len(st.units), "n0": args.n0,
                       "ms_per_step": ms, "TOPS": ops / (ms * 1e-3) / 1e12,
-                      "packed_weights_GiB": sum(l.n * ((l.k + 1) // 2) for l in ls) / 2**30}),
+                      "packed_weights_GiB": sum(l.n * ((l.k + 1) // 2) for l in ls) / 2**30,
+                      "device_layers_GiB_measured": st.layer_bytes / 2**30}),
           flush=True)
     del st
     torch.cuda.empty_cache()
