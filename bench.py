@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--path", choices=["v3", "v2"], default="v3",
                     help="K1+K3 pair: v3 (int8 codes, hardware weight expansion; what "
                          "forward() runs) or v2 (packed codes, software expansion)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config blocks (cfg1, cfg3 N0 sweep, cfg4 FLUX stack)")
+    ap.add_argument("--cpu-stages", type=int, default=0, metavar="ROWS",
+                    help=argparse.SUPPRESS)  # child process: staged CPU reference timing
     ap.add_argument("--parallel", choices=["replica", "column"], default="replica",
                     help="N>1: independent prompt replicas (weak scaling, default) or "
                          "column-parallel fc1/fc2 with an NCCL all-gather (strong scaling)")
@@ -115,6 +119,83 @@ class CpuReference:
 
     def tops(self, rows: int, seconds: float) -> float:
         return 2.0 * rows * (D_FF * D_MODEL + D_MODEL * D_FF) / seconds / 1e12
+
+
+def cpu_stages_child(rows: int) -> None:
+    """Child process (CONVROT_THREADS fixed for its lifetime, parallel.cpp:10-22):
+    the reference's stages on `rows` token rows of the fc1 / fc2 inputs --
+    group_rotate, compute_scales + quantize, int_gemm -- and the whole
+    forward_prepared, one warm-up and the median of 3 each."""
+    import numpy as np
+    ref = CpuReference(int(os.environ.get("CONVROT_THREADS", "1")))
+    O = ref.O
+    if ref.kind != "reference":
+        print(json.dumps({"kind": ref.kind}))
+        return
+    x = ref.x_all[:rows]
+    y1 = O.Ref.forward_prepared(x, ref.l1[0], ref.l1[1], ref.b1, O.ROT_REGULAR, N0)
+
+    def med3(fn):
+        fn()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    out = {"kind": "reference", "threads": ref.threads, "rows": rows, "stages_s": {}}
+    for name, xin, layer, k, n in (("fc1", x, ref.l1, D_MODEL, D_FF),
+                                   ("fc2", y1, ref.l2, D_FF, D_MODEL)):
+        rot = O.Ref.group_rotate(xin, O.ROT_REGULAR, N0)
+        sc = O.Ref.compute_scales(rot, 4)
+        codes = O.Ref.quantize(rot, sc, 4)
+        out["stages_s"][name] = {
+            "group_rotate": med3(lambda: O.Ref.group_rotate(xin, O.ROT_REGULAR, N0)),
+            "compute_scales+quantize": med3(lambda: O.Ref.quantize(rot, O.Ref.compute_scales(rot, 4), 4)),
+            "int_gemm": med3(lambda: O.Ref.int_gemm(codes, layer[0], 4, 4)),
+            "forward": med3(lambda: O.Ref.forward_prepared(xin, layer[0], layer[1], None,
+                                                           O.ROT_REGULAR, N0)),
+        }
+    fwd = out["stages_s"]["fc1"]["forward"] + out["stages_s"]["fc2"]["forward"]
+    out["forward_s"] = fwd
+    out["tops"] = 2.0 * rows * (D_FF * D_MODEL + D_MODEL * D_FF) / fwd / 1e12
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_staged(budget_s: float = 40.0):
+    """The reference CPU path on the box's host cores, per BASELINE.md 3:
+    CONVROT_THREADS = nproc and = 1 (each in its own process), per-stage
+    times, one warm-up and the median of 3, on a bounded row sample (rows
+    are independent: per-token scales).  ~budget_s of CPU work in total."""
+    nproc = os.cpu_count() or 1
+    res = {}
+    # cost model: one forward of one row ~ 12 ms / nproc-thread-GOPS; each
+    # child runs ~9 forward-equivalents (stages + forward, warm-up + 3)
+    for threads, share in ((nproc, 0.6), (1, 0.4)):
+        env = dict(os.environ, CONVROT_THREADS=str(threads))
+        probe = subprocess.run([sys.executable, __file__, "--cpu-stages", "16"], env=env,
+                               capture_output=True, text=True, timeout=600)
+        try:
+            p = json.loads(probe.stdout.strip().splitlines()[-1])
+        except Exception:
+            return {"value": None, "unit": "TOPS", "cores": 0, "kind": "unavailable",
+                    "sample": f"cpu stage child failed: {probe.stderr[-300:]}"}
+        if p.get("kind") != "reference":
+            return None
+        per_row = max(p["forward_s"] / 16, 1e-5)
+        rows = int(max(16, min(1024, budget_s * share / 9.0 / per_row)) // 16 * 16)
+        r = subprocess.run([sys.executable, __file__, "--cpu-stages", str(rows)], env=env,
+                           capture_output=True, text=True, timeout=900)
+        res[threads] = json.loads(r.stdout.strip().splitlines()[-1])
+    top = res[nproc]
+    one = res[1]
+    return {"value": top["tops"], "unit": "TOPS", "cores": top["threads"], "kind": "reference",
+            "sample": (f"{top['rows']} of {M_TOK} token rows through fc1+fc2 (forward_prepared), "
+                       f"CONVROT_THREADS={top['threads']}; one warm-up, median of 3"),
+            "stages_s": top["stages_s"],
+            "threads_1": {"value": one["tops"], "unit": "TOPS", "rows": one["rows"],
+                          "stages_s": one["stages_s"]}}
 
 
 def run_reference_arm(args):
@@ -203,6 +284,169 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(busy) if busy else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# Per-config blocks (BASELINE.json configs[0], [2], [3]) and device-only
+# kernel times: back-to-back launches captured in one CUDA graph, cycling
+# over enough input buffers that every K1 launch reads its input from HBM
+# (> 2x the 126 MB L2) -- launch gaps and host overhead excluded.
+# ---------------------------------------------------------------------------
+L2_BYTES = 126 * 1024 * 1024
+NOMINAL_INT8_TOPS = 4500.0
+
+
+def graph_us(calls, reps: int, dev) -> float:
+    import torch
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        for c in calls:  # plans, attributes, tensor maps
+            c()
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for _ in range(reps):
+            for c in calls:
+                c()
+    g.replay()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3 / (reps * len(calls)))
+    del g
+    return statistics.median(ts)
+
+
+class KernelRig:
+    """Device buffers for timing K1 (int8-code production layout) and K3 v3
+    at one (M, K, N) through the C-ABI."""
+
+    def __init__(self, lib, abi, dev, M, K, N=None, seed=5):
+        import ctypes
+        import torch
+        self.lib, self.abi, self.dev, self.M, self.K, self.N = lib, abi, dev, M, K, N
+        self.ct = ctypes
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.nbuf = max(2, -(-3 * L2_BYTES // (M * K * 2)))
+        self.x = [torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+                  for _ in range(self.nbuf)]
+        self.ld = (K + 15) // 16 * 16
+        self.codes = [torch.empty(M, self.ld, dtype=torch.uint8, device=dev) for _ in range(self.nbuf)]
+        self.s = [torch.empty(M, dtype=torch.float32, device=dev) for _ in range(self.nbuf)]
+        self.sums = [torch.empty(M, dtype=torch.int32, device=dev) for _ in range(self.nbuf)]
+        self.y = torch.empty(M, N or 1, dtype=torch.bfloat16, device=dev) if N else None
+
+    def _sp(self):
+        import torch
+        return self.ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def k1(self, i, rc):
+        P = lambda t: self.ct.c_void_p(t.data_ptr())  # noqa: E731
+        self.abi.check(self.lib.crt_rotate_quant_i8(
+            P(self.x[i]), self.abi.CRT_DTYPE_BF16, self.M, self.K, self.K, self.ct.byref(rc),
+            P(self.codes[i]), self.ld, P(self.s[i]), P(self.sums[i]), self._sp()))
+
+    def k3(self, i, layer):
+        P = lambda t: self.ct.c_void_p(t.data_ptr())  # noqa: E731
+        self.abi.check(self.lib.crt_quant_gemm_i8(
+            P(self.codes[i]), self.ld, P(self.s[i]), P(self.sums[i]), layer.handle, self.M,
+            self.abi.CRT_OUT_BF16, P(self.y), self.N, self._sp()))
+
+    def k1_block(self, n0, hbm):
+        from paper_2512_03673_b200 import RotationKind, RotationSpec
+        rc = RotationSpec(RotationKind.regular, n0).c()
+        us = graph_us([lambda i=i: self.k1(i, rc) for i in range(self.nbuf)],
+                      max(2, 96 // self.nbuf), self.dev)
+        packed = self.M * self.K * 2.5 + 4 * self.M  # SURVEY.md 8(d) algorithmic bytes
+        moved = self.M * self.K * 3 + 8 * self.M      # int8 codes + scale + code sum
+        return {"n0": n0, "us": us, "GBps_packed": packed / us / 1e3,
+                "frac_packed": packed / us / 1e3 / hbm, "GBps_moved": moved / us / 1e3,
+                "bytes_packed": packed}
+
+    def k3_block(self, layer, int8_peak, n0):
+        from paper_2512_03673_b200 import RotationKind, RotationSpec
+        rc = RotationSpec(RotationKind.regular, n0).c()
+        for i in range(self.nbuf):
+            self.k1(i, rc)
+        us = graph_us([lambda i=i: self.k3(i, layer) for i in range(self.nbuf)],
+                      max(2, 24 // self.nbuf), self.dev)
+        ops = 2 * self.M * self.N * self.K
+        tops = ops / us / 1e6
+        fwd = graph_us([c for i in range(self.nbuf)
+                        for c in (lambda i=i: self.k1(i, rc), lambda i=i: self.k3(i, layer))],
+                       max(2, 24 // self.nbuf), self.dev) * 2
+        return {"k3_us": us, "k3_TOPS": tops, "k3_frac_measured_int8": tops / int8_peak,
+                "k3_frac_nominal_int8": tops / NOMINAL_INT8_TOPS, "forward_us": fwd,
+                "forward_TOPS": ops / fwd / 1e6}
+
+
+def per_config_blocks(crt, lib, abi, dev, int8_peak, hbm):
+    """cfg2's K1 roofline (both layers), cfg1 (attn-proj 4096x3072x3072),
+    cfg3 (N0 sweep at 4608x3072x3072) and cfg4 (the FLUX.1-dev linear stack)."""
+    import torch
+    from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec
+    out = {"timing": ("device-only: back-to-back launches in one CUDA graph over input buffers "
+                      "> 2x L2 (every K1 reads HBM); forward = K1 + K3 pairs")}
+    gw = torch.Generator(device=dev).manual_seed(7)
+    # cfg2 K1 (the headline pair's rotate+quant kernels)
+    out["cfg2_k1"] = {}
+    for name, K in (("fc1", D_MODEL), ("fc2", D_FF)):
+        rig = KernelRig(lib, abi, dev, M_TOK, K)
+        out["cfg2_k1"][name] = rig.k1_block(N0, hbm)
+        del rig
+    # cfg1: single ConvLinear4bit forward, attn-proj M=4096, K=N=3072
+    w = torch.randn(D_MODEL, D_MODEL, device=dev, generator=gw).to(torch.bfloat16)
+    b = torch.randn(D_MODEL, device=dev, generator=gw)
+    rig = KernelRig(lib, abi, dev, 4096, D_MODEL, D_MODEL)
+    layer = crt.prepare_layer(w, b, RotationSpec(RotationKind.regular, N0), QuantSpec(4), "cfg1")
+    out["cfg1"] = {"workload": "M=4096, K=N=3072, N0=16 (configs[0])", **rig.k1_block(N0, hbm),
+                   **rig.k3_block(layer, int8_peak, N0)}
+    del rig, layer
+    # cfg3: N0 sweep at M=4608, K=N=3072
+    rig = KernelRig(lib, abi, dev, M_TOK, D_MODEL, D_MODEL)
+    sweep = []
+    for n0 in (4, 16, 64, 256):
+        layer = crt.prepare_layer(w, b, RotationSpec(RotationKind.regular, n0), QuantSpec(4), "cfg3")
+        blk = rig.k1_block(n0, hbm)
+        blk.update(rig.k3_block(layer, int8_peak, n0))
+        sweep.append(blk)
+        del layer
+    out["cfg3"] = {"workload": "M=4608, K=N=3072, N0 in {4,16,64,256} (configs[2])",
+                   "per_n0": sweep}
+    del rig, w
+    torch.cuda.empty_cache()
+    # cfg4: the 494-linear FLUX.1-dev stack, siblings fused, text stream on a
+    # second CUDA stream (paper_2512_03673_b200/flux.py)
+    from paper_2512_03673_b200.flux import FluxStack, flux_linears, stack_ops
+    ls = flux_linears()
+    stk = FluxStack(ls, fused=True, n0=N0, streams=2, device=dev)
+    for _ in range(2):
+        stk.step()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(5):
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        stk.step()
+        e.record()
+        e.synchronize()
+        ts.append(a.elapsed_time(e))
+    ms = statistics.median(ts)
+    tops = stack_ops(ls) / (ms * 1e-3) / 1e12
+    out["cfg4"] = {"workload": "FLUX.1-dev linear stack, 19 double + 38 single blocks, 494 linears "
+                               "(304 fused units), N0=16, W4A4 (configs[3])",
+                   "ms_per_step": ms, "TOPS": tops, "frac_measured_int8": tops / int8_peak,
+                   "frac_nominal_int8": tops / NOMINAL_INT8_TOPS,
+                   "device_layers_GiB": stk.layer_bytes / 2**30,
+                   "timing": "median of 5 steps, CUDA events around each step (L2 warm)"}
+    del stk
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -462,20 +706,31 @@ def run_ours(args):
                "ms_per_step": e_ms, "pipelined_streams": NB,
                "step_latency_ms": statistics.median(lat)}
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs and not args.profile:
+        configs = per_config_blocks(crt, lib, _abi, dev, int8_peak, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
-            ref = CpuReference(os.cpu_count() or 1)
-            rows = ref.calibrate(target_s=12.0, max_rows=2048)
-            t = ref.step(rows)
-            cpu = {"value": ref.tops(rows, t), "unit": "TOPS", "cores": ref.threads,
-                   "kind": ref.kind,
-                   "sample": f"{rows} of {M_TOK} token rows through fc1+fc2 (one timed pass, "
-                             f"{t:.1f} s; CONVROT_THREADS={ref.threads})"}
+            cpu = cpu_baseline_staged()
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "TOPS", "cores": 0, "kind": "unavailable",
                    "sample": f"error: {exc}"}
 
+    if configs is not None:
+        c2 = configs["cfg2_k1"]
+        k1_roof = {"bound": "hbm", "kernel": "k1_team (rotate + quantise, int8 codes + row sums)",
+                   "achieved": c2["fc2"]["GBps_packed"], "peak": hbm, "unit": "GB/s",
+                   "frac": c2["fc2"]["frac_packed"], "fc1_gbs": c2["fc1"]["GBps_packed"],
+                   "fc1_frac": c2["fc1"]["frac_packed"],
+                   "bytes": "SURVEY.md 8(d): M*K*(2 B bf16 in + 0.5 B packed codes) + 4 B/row",
+                   "us": {k: v["us"] for k, v in c2.items()},
+                   "timing": configs["timing"]}
+    else:
+        k1_roof = {"bound": "hbm", "achieved": k1_gbs["fc2"], "peak": hbm, "unit": "GB/s",
+                   "frac": k1_gbs["fc2"] / hbm, "fc1_gbs": k1_gbs["fc1"],
+                   "bytes_per_launch": k1_bytes, "timing": "event-bracketed launches"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
@@ -494,16 +749,18 @@ def run_ours(args):
                                    "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
                          "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",
                          "frac": k3_tops / int8_peak, "traffic": traffic,
+                         "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per fc1 "
+                                            "launch from an ncu --set full capture "
+                                            "(profiles/k3_traffic.json); not measured in this run"),
                          "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json); "
                                       f"vs nominal 4500: {k3_tops / 4500:.3f}",
                          "ops_per_launch": k3_ops_per_launch, "avg_launch_us": k3_us},
-            "k1_roofline": {"bound": "hbm", "achieved": k1_gbs["fc2"], "peak": hbm, "unit": "GB/s",
-                            "frac": k1_gbs["fc2"] / hbm, "fc1_gbs": k1_gbs["fc1"],
-                            "bytes_per_launch": k1_bytes},
+            "k1_roofline": k1_roof,
             "kernels_us": {k: statistics.mean(v) * 1e3 for k, v in seg.items()},
             "kernels_note": "kernels_us and roofline.avg_launch_us come from a second pass of the "
                             "same steps with an event between kernels; ms_per_step from the timed "
                             "pass with events only at step boundaries (PDL overlap kept)",
+            "configs": configs,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clocks.summary(), "wall_s_timed": wall,
         }
@@ -514,6 +771,9 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.cpu_stages:
+        cpu_stages_child(args.cpu_stages)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
         return
