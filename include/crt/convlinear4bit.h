@@ -42,7 +42,8 @@ typedef enum crt_status {
   CRT_ERR_CAPACITY = 4,      /* CapacityError     (errors.hpp:37-41) */
   CRT_ERR_FORMAT = 5,        /* FormatError       (errors.hpp:43-54) */
   CRT_ERR_CUDA = 6,          /* CUDA runtime/driver failure */
-  CRT_ERR_UNSUPPORTED = 7    /* valid for the reference, not built here */
+  CRT_ERR_UNSUPPORTED = 7,   /* valid for the reference, not built here */
+  CRT_ERR_NCCL = 8           /* NCCL unavailable or a collective failed (crt_tp_*) */
 } crt_status;
 
 /* RotationKind (pipeline.hpp:14); random_orthogonal is out of scope. */
@@ -241,6 +242,11 @@ typedef struct crt_workspace crt_workspace;
 
 crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** out);
 crt_status crt_workspace_destroy(crt_workspace* ws);
+/* Non-finite input seen by forwards run with this workspace (its own error
+ * word: other callers' inputs never show up here).  Synchronises `stream`;
+ * INVALID_VALUE (compute_scales, quant.cpp:16-18) if set, then clears it
+ * when reset != 0. */
+crt_status crt_workspace_status(crt_workspace* ws, void* stream, int32_t reset);
 
 crt_status crt_forward(const crt_layer* layer, const void* x, int32_t x_dtype,
                        int64_t M, int64_t ldx, int32_t bits_a, int32_t out_kind,
@@ -252,6 +258,54 @@ crt_status crt_forward(const crt_layer* layer, const void* x, int32_t x_dtype,
 crt_status crt_forward_host(const crt_layer* layer, const void* x_host, int32_t x_dtype,
                             int64_t M, int32_t bits_a, int32_t out_kind, void* y_host,
                             void* x_dev, void* y_dev, crt_workspace* ws, void* stream);
+
+
+/* -------------------------------------------------------------------------
+ * Tensor parallelism over NCCL (SURVEY.md 8(b) "Multi-GPU", 8(e)): one
+ * process per GPU.  The collectives are NCCL's, resolved at first use from
+ * the libnccl.so.2 already loaded in the process (e.g. PyTorch's) or the
+ * system one -- so a communicator made by the caller's NCCL may be passed.
+ * `comm` is an ncclComm_t passed as void*.  NCCL missing or a failing
+ * collective -> CRT_ERR_NCCL.
+ *
+ *   CRT_TP_COLUMN  rank r of P owns output channels [r*N/P, (r+1)*N/P) (the
+ *                  full layer's rows: codes, scales, bias); x is the full
+ *                  [M, K] input on every rank.  crt_tp_forward runs K1 + K3
+ *                  on the shard and, with gather != 0, all-gathers the shards
+ *                  into y [M, N] (rank-major NCCL buffer interleaved by a
+ *                  kernel); gather == 0 leaves the rank's [M, N/P] columns in
+ *                  y -- the input shard of a following CRT_TP_ROW layer.
+ *   CRT_TP_ROW     rank r owns input features [r*K/P, (r+1)*K/P) (per-channel
+ *                  scales over all of K); x is the rank's [M, K/P] shard.
+ *                  crt_tp_forward: exact per-row max |group_rotate| of the
+ *                  shard, MAX all-reduce (M doubles), K1 with the global max
+ *                  (codes = the unsharded ones), K3 partial int32
+ *                  accumulators, SUM all-reduce (exact, order-free), dequant
+ *                  -> y [M, N] on every rank.
+ * Both equal the single-GPU forward bit for bit. */
+typedef enum crt_tp_mode { CRT_TP_COLUMN = 1, CRT_TP_ROW = 2 } crt_tp_mode;
+
+/* NCCL bootstrap for hosts without their own: a 128-byte ncclUniqueId made
+ * on one rank and shared with the others by any transport, then one
+ * communicator per rank on the CURRENT device. */
+crt_status crt_nccl_unique_id(uint8_t* id128);
+crt_status crt_nccl_comm_create(int32_t nranks, int32_t rank, const uint8_t* id128, void** comm);
+crt_status crt_nccl_comm_destroy(void* comm);
+/* rank / size of a communicator (ncclCommUserRank / ncclCommCount). */
+crt_status crt_nccl_comm_info(void* comm, int32_t* rank, int32_t* nranks);
+
+/* The rank's shard of a layer (rank and P from `comm`); SHAPE if N (column)
+ * or K (row) is not divisible by P, or a rotation group would straddle
+ * K shards. */
+crt_status crt_tp_layer_prepare(const crt_layer_desc* desc, const void* w, int64_t ldw,
+                                const float* bias, int32_t mode, void* comm, void* stream,
+                                crt_layer** out);
+/* Forward of a crt_tp_layer_prepare layer (see above); W4A4 / W8A8 as the
+ * layer's bits.  Collective: every rank of `comm` must call it.  Scratch for
+ * the gathered / reduced buffers is stream-ordered (cudaMallocAsync). */
+crt_status crt_tp_forward(const crt_layer* layer, const void* x, int32_t x_dtype, int64_t M,
+                          int64_t ldx, int32_t out_kind, void* y, int64_t ldy, int32_t gather,
+                          crt_workspace* ws, void* comm, void* stream);
 
 /* -------------------------------------------------------------------------
  * Diagnostics. */

@@ -162,6 +162,12 @@ class Workspace {
     if (h_) crt_workspace_destroy(h_);
   }
   crt_workspace* handle() const { return h_; }
+  // Raises InvalidValueError if a forward run with this workspace saw a
+  // non-finite input (compute_scales, quant.cpp:16-18); its own error word.
+  // Synchronises the stream.
+  void status(void* stream = nullptr, bool reset = true) {
+    check(crt_workspace_status(h_, stream, reset ? 1 : 0));
+  }
 
  private:
   crt_workspace* h_ = nullptr;
@@ -224,8 +230,10 @@ inline void forward(const void* x, DType dt, int64_t m, int64_t ldx, const Prepa
                     static_cast<int32_t>(out), y, ldy, ws.handle(), stream));
 }
 
-// Raises InvalidValueError if a kernel saw a non-finite input
-// (compute_scales, quant.cpp:16-18).  Synchronises the stream.
+// Raises InvalidValueError if a free-standing K1 call (rotate_quantize*,
+// rotated_row_absmax) saw a non-finite input (compute_scales,
+// quant.cpp:16-18).  Forwards report through Workspace::status;
+// prepare_layer throws by itself.  Synchronises the stream.
 inline void device_status(void* stream = nullptr, bool reset = true) {
   check(crt_device_status(stream, reset ? 1 : 0));
 }

@@ -23,6 +23,8 @@ CRT_ERR_CAPACITY = 4
 CRT_ERR_FORMAT = 5
 CRT_ERR_CUDA = 6
 CRT_ERR_UNSUPPORTED = 7
+CRT_ERR_NCCL = 8
+CRT_TP_COLUMN, CRT_TP_ROW = 1, 2
 
 CRT_DTYPE_BF16, CRT_DTYPE_F32 = 0, 1
 CRT_OUT_BF16, CRT_OUT_F32, CRT_OUT_I32_ACC = 0, 1, 2
@@ -61,8 +63,14 @@ class UnsupportedError(Error):
     status = CRT_ERR_UNSUPPORTED
 
 
+class NcclError(Error):
+    """NCCL unavailable or a collective failed (crt_tp_*; no reference
+    counterpart: the reference is single-process)."""
+    status = CRT_ERR_NCCL
+
+
 _EXC = {c.status: c for c in (InvalidOrderError, InvalidValueError, ShapeError, CapacityError,
-                              FormatError, CudaError, UnsupportedError)}
+                              FormatError, CudaError, UnsupportedError, NcclError)}
 
 
 class RotationSpecC(ctypes.Structure):
@@ -114,6 +122,14 @@ _SIGS = {
     "crt_forward": (_I32, [_P, _P, _I32, _I64, _I64, _I32, _I32, _P, _I64, _P, _P]),
     "crt_forward_host": (_I32, [_P, _P, _I32, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "crt_device_status": (_I32, [_P, _I32]),
+    "crt_workspace_status": (_I32, [_P, _P, _I32]),
+    "crt_nccl_unique_id": (_I32, [_P]),
+    "crt_nccl_comm_create": (_I32, [_I32, _I32, _P, ctypes.POINTER(_P)]),
+    "crt_nccl_comm_destroy": (_I32, [_P]),
+    "crt_nccl_comm_info": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "crt_tp_layer_prepare": (_I32, [ctypes.POINTER(LayerDescC), _P, _I64, _P, _I32, _P, _P,
+                                    ctypes.POINTER(_P)]),
+    "crt_tp_forward": (_I32, [_P, _P, _I32, _I64, _I64, _I32, _P, _I64, _I32, _P, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -8,6 +8,7 @@ memory and the current stream.
 from __future__ import annotations
 
 import ctypes
+import threading
 import enum
 from dataclasses import dataclass
 from typing import Optional, Tuple
@@ -218,7 +219,8 @@ def _prepare(w, bias, rotation, wq, name, rank, nranks, kshard=False):
         else:
             check(_lib().crt_layer_prepare_shard(ctypes.byref(desc), _ptr(w), w.stride(0),
                                                  _ptr(bias), rank, nranks, st, ctypes.byref(h)))
-        check(_lib().crt_device_status(st, 1))
+        # non-finite weights: the C-ABI reports them synchronously
+        # (compute_scales throws, quant.cpp:16-18)
     if kshard:
         return PreparedLayer(h.value, N, K // nranks, rotation, wq, bias is not None, name,
                              w.device, (rank, nranks))
@@ -262,6 +264,12 @@ class Workspace:
     def handle(self):
         return self._h
 
+    def status(self, reset: bool = True) -> None:
+        """Raise InvalidValueError if a forward run with this workspace saw a
+        non-finite input (its own error word; synchronises the stream)."""
+        with torch.cuda.device(self.device):
+            check(_lib().crt_workspace_status(self._h, _stream(), int(reset)))
+
     def close(self):
         if self._h is not None and self._h.value:
             _lib().crt_workspace_destroy(self._h)
@@ -275,10 +283,18 @@ class Workspace:
 
 
 _ws_cache = {}
+_ws_lock = threading.Lock()
 
 
 def _workspace_for(M: int, K: int, device) -> Workspace:
-    key = (str(device),)
+    """The default workspace of (device, current stream): forwards on
+    different streams never share activation-code scratch."""
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    with _ws_lock:
+        return _workspace_locked(key, M, K, device)
+
+
+def _workspace_locked(key, M: int, K: int, device) -> Workspace:
     ws = _ws_cache.get(key)
     if ws is None or ws.max_m < M or ws.max_k < K:
         ws = Workspace(max(M, ws.max_m if ws else 0), max(K, ws.max_k if ws else 0), device)
@@ -286,28 +302,61 @@ def _workspace_for(M: int, K: int, device) -> Workspace:
     return ws
 
 
+def _same_device(a, b) -> bool:
+    a, b = torch.device(a), torch.device(b)
+    if a.type != b.type:
+        return False
+    cur = torch.cuda.current_device() if a.type == "cuda" else 0
+    return (cur if a.index is None else a.index) == (cur if b.index is None else b.index)
+
+
+def _check_out(y: torch.Tensor, M: int, N: int, out: str, device) -> None:
+    """A caller-supplied output buffer must be exactly what the kernels write:
+    the out kind's dtype, [M, N] (row pitch >= N), unit column stride, on the
+    layer's device."""
+    if y.dtype != _OUT_DTYPE[out]:
+        raise InvalidValueError(f"y must be {_OUT_DTYPE[out]} for out={out!r}, got {y.dtype}")
+    if y.dim() != 2 or tuple(y.shape) != (M, N) or y.stride(1) != 1 or y.stride(0) < N:
+        raise ShapeError(f"y must be a row-major [{M}, {N}] matrix, got {tuple(y.shape)} "
+                         f"strides {y.stride()}")
+    if not _same_device(y.device, device):
+        raise InvalidValueError(f"y is on {y.device}, the layer on {device}")
+
+
 def forward(x: torch.Tensor, layer: PreparedLayer, aq: QuantSpec = QuantSpec(4), *,
             out: str = "bf16", y: Optional[torch.Tensor] = None,
-            workspace: Optional[Workspace] = None, check_finite: bool = False) -> torch.Tensor:
+            workspace: Optional[Workspace] = None, check_finite: bool = True) -> torch.Tensor:
     """Online half of ConvLinear4bit (pipeline.cpp:206-233): rotate x,
     per-token quantize, integer GEMM against the prepared weights, dequantize
     by s_a[m]*s_w[n], add bias.  ``out``: "bf16" (production), "f32"
-    (dequant parity) or "i32" (raw int_gemm accumulators)."""
+    (dequant parity) or "i32" (raw int_gemm accumulators).
+
+    Non-finite input raises InvalidValueError like the reference
+    (compute_scales, quant.cpp:16-18): with ``check_finite`` (default) the
+    call synchronises the stream and reads the workspace's own error word.
+    Pipelined callers pass ``check_finite=False`` and poll
+    ``workspace.status()`` when convenient."""
     _check_2d_cuda(x, "x")
     M, K = x.shape
     if K != layer.in_features:  # pipeline.cpp:208-212
         raise ShapeError(f"forward: input has {K} columns, layer expects {layer.in_features}")
     if aq.bits not in (4, 8):  # :213-215
         raise InvalidValueError("forward: activation bits must be 4 or 8")
+    if not _same_device(x.device, layer.device):
+        raise InvalidValueError(f"x is on {x.device}, the layer on {layer.device}")
     N = layer.out_features
     if y is None:
         y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=x.device)
+    else:
+        _check_out(y, M, N, out, layer.device)
     ws = workspace or _workspace_for(M, K, x.device)
+    if ws.max_m < M or ws.max_k < K:
+        raise ShapeError("workspace too small")
     st = _stream(x)
     check(_lib().crt_forward(layer.handle, _ptr(x), _dtype_code(x), M, x.stride(0), aq.bits,
                              _OUT[out], _ptr(y), y.stride(0), ws.handle, st))
     if check_finite:
-        check(_lib().crt_device_status(st, 1))
+        check(_lib().crt_workspace_status(ws.handle, st, 1))
     return y
 
 
@@ -319,6 +368,8 @@ def quant_gemm(codes: torch.Tensor, scales: torch.Tensor, layer: PreparedLayer,
     N = layer.out_features
     if y is None:
         y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=codes.device)
+    else:
+        _check_out(y, M, N, out, layer.device)
     check(_lib().crt_quant_gemm(_ptr(codes), codes.stride(0), _ptr(scales), aq.bits, layer.handle,
                                 M, _OUT[out], _ptr(y), y.stride(0), _stream(codes)))
     return y
@@ -372,6 +423,8 @@ def dequant(acc: torch.Tensor, scales: torch.Tensor, layer: PreparedLayer, *, ou
     M = acc.shape[0]
     if y is None:
         y = torch.empty((M, layer.out_features), dtype=_OUT_DTYPE[out], device=acc.device)
+    else:
+        _check_out(y, M, layer.out_features, out, layer.device)
     check(_lib().crt_dequant(_ptr(acc), acc.stride(0), M, _ptr(scales), layer.handle, _OUT[out],
                              _ptr(y), y.stride(0), _stream(acc)))
     return y
@@ -386,6 +439,8 @@ def quant_gemm_i8(codes: torch.Tensor, scales: torch.Tensor, sums: torch.Tensor,
     N = layer.out_features
     if y is None:
         y = torch.empty((M, N), dtype=_OUT_DTYPE[out], device=codes.device)
+    else:
+        _check_out(y, M, N, out, layer.device)
     check(_lib().crt_quant_gemm_i8(_ptr(codes), codes.stride(0), _ptr(scales), _ptr(sums),
                                    layer.handle, M, _OUT[out], _ptr(y), y.stride(0),
                                    _stream(codes)))

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -15,25 +16,31 @@
 
 #include "../../include/crt/convlinear4bit.h"
 #include "common.cuh"
+#include "crt_internal.h"
 #include "k1_rotate_quant.h"
 #include "k3_gemm.h"
 
-namespace {
+namespace crt_detail {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 
-// One device error word per device (lazily allocated, never freed).
+// One device error word per device for the free-standing K1 entry points
+// (crt_rotate_quant*, crt_device_status), lazily allocated under a mutex,
+// never freed.  Forward calls use their workspace's own word and layer
+// preparation a per-call word (crt_workspace_status, prepare_impl).
 int* device_error_word() {
   static int* words[64] = {nullptr};
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
   if (!words[dev]) {
     int* p = nullptr;
     if (cudaMalloc(&p, sizeof(int)) != cudaSuccess) return nullptr;
-    cudaMemset(p, 0, sizeof(int));
-    cudaDeviceSynchronize();
+    const int zero = 0;
+    if (cudaMemcpy(p, &zero, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
     words[dev] = p;
   }
   return words[dev];
@@ -89,8 +96,8 @@ crt_status resolve_rotation(const crt_rotation_spec* rot, int64_t cols, int64_t*
 
 crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                   const crt_rotation_spec* rot, int32_t bits, uint8_t* codes, int64_t ldc,
-                  float* s32, double* s64, cudaStream_t st, double* amax = nullptr,
-                  int32_t* rowsum = nullptr, const double* amax_in = nullptr) {
+                  float* s32, double* s64, cudaStream_t st, double* amax,
+                  int32_t* rowsum, const double* amax_in, int* err) {
   // bits 5 (internal): 4-bit codes stored one int8 per code, + row code sums
   if (x_dtype != CRT_DTYPE_BF16 && x_dtype != CRT_DTYPE_F32)
     return fail(CRT_ERR_INVALID_VALUE, "unsupported input dtype");
@@ -110,9 +117,18 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
   }
   if (ldx < K) return fail(CRT_ERR_SHAPE, "ldx < K");
   const int64_t row_bytes = bits == 4 ? (K + 1) / 2 : K;  // bits 5, 8: one byte per code
-  if (ldc < row_bytes) return fail(CRT_ERR_SHAPE, "ld_codes too small for one packed row");
-  if (x == nullptr || codes == nullptr) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
+  if (x == nullptr) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
   const bool f32 = x_dtype == CRT_DTYPE_F32;
+  // amax only (codes == null): the team kernel skips the code stores; other
+  // kernels quantise into a stream-ordered scratch buffer
+  uint8_t* scratch = nullptr;
+  const bool amax_only = codes == nullptr;
+  if (amax_only) {
+    if (!amax || rowsum) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
+    ldc = 16;
+  } else if (ldc < row_bytes) {
+    return fail(CRT_ERR_SHAPE, "ld_codes too small for one packed row");
+  }
   const int kind = rot ? rot->kind : CRT_ROT_NONE;
   crt::K1Args a{};
   a.x = x;
@@ -129,39 +145,29 @@ crt_status run_k1(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t 
   a.amax = amax;
   a.rowsum = rowsum;
   a.amax_in = amax_in;
-  a.err = device_error_word();
+  a.err = err ? err : device_error_word();
   if (!a.err) return fail(CRT_ERR_CUDA, "device error word allocation failed");
   crt::K1Plan plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx,
                                   codes, ldc);
+  if (amax_only && !(plan.fast && crt::k1_team_eligible(a, f32, bits))) {
+    a.ldc = (row_bytes + 15) / 16 * 16;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)a.ldc * M, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch alloc");
+    a.codes = scratch;
+    plan = crt::plan_k1(K, group, kind, rot && rot->identity_tail, f32, bits, x, ldx, scratch,
+                        a.ldc);
+  }
   int64_t launches = 0;
   cudaError_t e = crt::launch_k1(a, plan, f32, bits, st, &launches);
   g_launches += launches;
+  if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "rotate_quant launch");
   return CRT_OK;
 }
 
-}  // namespace
+}  // namespace crt_detail
 
-// ---------------------------------------------------------------------------
-struct crt_layer {
-  crt_layer_desc desc;
-  int64_t n_total;      // N of the full layer (== desc.out_features unless sharded)
-  int64_t row_offset;   // first output channel of this shard
-  uint8_t* codes;       // bits 8: N x ldc int8 codes (K3's operand); bits 4: null --
-                        // the only copy is tiles' offset-binary one
-  int64_t ldc;          // reference-layout row pitch (scratch / export layout)
-  float* s32;           // N
-  double* s64;          // N
-  float* bias;          // N or null
-  crt::K3Weights tiles; // K3 operand layout
-};
-
-struct crt_workspace {
-  int64_t max_m, max_k;
-  uint8_t* codes;
-  float* s32;
-  int32_t* rowsum;
-};
+using namespace crt_detail;
 
 extern "C" {
 
@@ -234,15 +240,9 @@ crt_status crt_rotated_row_absmax(const void* x, int32_t x_dtype, int64_t M, int
                                   void* stream) {
   if (!amax_rows) return fail(CRT_ERR_INVALID_VALUE, "null output");
   if (M <= 0 || K <= 0) return fail(CRT_ERR_SHAPE, "outlier_amplitude: empty matrix");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t ldc = ((K + 1) / 2 + 15) / 16 * 16;
-  uint8_t* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, (size_t)ldc * M, st);
-  if (e != cudaSuccess) return cuda_fail(e, "scratch alloc");
-  crt_status r = run_k1(x, x_dtype, M, K, ldx, rot, 4, scratch, ldc, nullptr, nullptr, st,
-                        amax_rows);
-  cudaFreeAsync(scratch, st);
-  return r;
+  // amax-only K1 (no code stores where the team kernel applies)
+  return run_k1(x, x_dtype, M, K, ldx, rot, 4, nullptr, 0, nullptr, nullptr, (cudaStream_t)stream,
+                amax_rows);
 }
 
 crt_status crt_device_status(void* stream, int32_t reset) {
@@ -261,7 +261,9 @@ crt_status crt_device_status(void* stream, int32_t reset) {
 // ---------------------------------------------------------------------------
 // K2: prepare_layer (pipeline.cpp:158-176)
 // ---------------------------------------------------------------------------
-static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t ldw,
+}  // extern "C"
+
+crt_status crt_detail::prepare_impl(const crt_layer_desc* d, const void* w, int64_t ldw,
                                const float* bias, int32_t rank, int32_t nranks,
                                cudaStream_t st, crt_layer** out) {
   if (!d || !out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
@@ -308,9 +310,27 @@ static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t l
     return cuda_fail(e, "layer alloc");
   }
   // K1 on the weight rows: rotation along K, per-output-channel scales.
+  // Non-finite weights are reported synchronously, as compute_scales throws
+  // (quant.cpp:16-18), through a word of this call's own.
+  int* err = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&err), sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int), st);
+  if (e != cudaSuccess) {
+    drop_scratch();
+    crt_layer_destroy(L);
+    return cuda_fail(e, "error word");
+  }
   const char* wbase = reinterpret_cast<const char*>(w) + off * ldw * esz;
   crt_status s = run_k1(wbase, d->w_dtype, Ns, K, ldw, &d->rotation, d->bits_w, wcodes, L->ldc,
-                        L->s32, L->s64, st);
+                        L->s32, L->s64, st, nullptr, nullptr, nullptr, err);
+  int bad = 0;
+  if (s == CRT_OK) {
+    e = cudaMemcpyAsync(&bad, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) s = cuda_fail(e, "prepare_layer status");
+    else if (bad) s = fail(CRT_ERR_INVALID_VALUE, "compute_scales: non-finite weight");
+  }
+  cudaFreeAsync(err, st);
   if (s != CRT_OK) {
     drop_scratch();
     crt_layer_destroy(L);
@@ -327,6 +347,8 @@ static crt_status prepare_impl(const crt_layer_desc* d, const void* w, int64_t l
   *out = L;
   return CRT_OK;
 }
+
+extern "C" {
 
 // f2: a layer prepared elsewhere (reference save_prepared_layer,
 // pipeline.cpp:257-314): codes already rotated + quantised, given on the host
@@ -522,7 +544,9 @@ crt_status crt_layer_export(const crt_layer* L, uint8_t* codes, int64_t ld_codes
 // ---------------------------------------------------------------------------
 // K3 + forward
 // ---------------------------------------------------------------------------
-static crt_status quant_gemm_impl(const uint8_t* a_codes, int64_t lda, const float* a_scales,
+}  // extern "C"
+
+crt_status crt_detail::quant_gemm_impl(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                                   const int32_t* a_sums, int32_t layout, int32_t bits_a,
                                   const crt_layer* L, int64_t M, int32_t out_kind, void* y,
                                   int64_t ldy, void* stream) {
@@ -565,6 +589,8 @@ static crt_status quant_gemm_impl(const uint8_t* a_codes, int64_t lda, const flo
   if (e != cudaSuccess) return cuda_fail(e, "quant_gemm launch");
   return CRT_OK;
 }
+
+extern "C" {
 
 crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                           int32_t bits_a, const crt_layer* L, int64_t M, int32_t out_kind,
@@ -641,10 +667,14 @@ crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** ou
   cudaError_t e = cudaMalloc(&w->codes, (size_t)ld * (max_m ? max_m : 1));
   if (e == cudaSuccess) e = cudaMalloc(&w->s32, 4 * (size_t)(max_m ? max_m : 1));
   if (e == cudaSuccess) e = cudaMalloc(&w->rowsum, 4 * (size_t)(max_m ? max_m : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&w->err, sizeof(int));
+  const int zero = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(w->err, &zero, sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(w->codes);
     cudaFree(w->s32);
     cudaFree(w->rowsum);
+    cudaFree(w->err);
     delete w;
     return cuda_fail(e, "workspace alloc");
   }
@@ -657,7 +687,24 @@ crt_status crt_workspace_destroy(crt_workspace* w) {
   cudaFree(w->codes);
   cudaFree(w->s32);
   cudaFree(w->rowsum);
+  cudaFree(w->err);
   delete w;
+  return CRT_OK;
+}
+
+crt_status crt_workspace_status(crt_workspace* w, void* stream, int32_t reset) {
+  if (!w) return fail(CRT_ERR_INVALID_VALUE, "null workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  int v = 0;
+  cudaError_t e = cudaMemcpyAsync(&v, w->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "workspace_status");
+  if (reset && v) {
+    e = cudaMemsetAsync(w->err, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace_status reset");
+  }
+  if (v) return fail(CRT_ERR_INVALID_VALUE, "compute_scales: non-finite input");
   return CRT_OK;
 }
 
@@ -673,14 +720,14 @@ crt_status crt_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64
     // v3: int8-stored codes + code sums -> hardware-expanded weights GEMM
     const int64_t ldc = (K + 15) / 16 * 16;
     crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, 5, ws->codes, ldc, ws->s32,
-                          nullptr, (cudaStream_t)stream, nullptr, ws->rowsum);
+                          nullptr, (cudaStream_t)stream, nullptr, ws->rowsum, nullptr, ws->err);
     if (s != CRT_OK) return s;
     return quant_gemm_impl(ws->codes, ldc, ws->s32, ws->rowsum, 1, 4, L, M, out_kind, y, ldy,
                            stream);
   }
   const int64_t ldc = bits_a == 4 ? ((K + 1) / 2 + 15) / 16 * 16 : (K + 15) / 16 * 16;
   crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, bits_a, ws->codes, ldc, ws->s32,
-                        nullptr, (cudaStream_t)stream);
+                        nullptr, (cudaStream_t)stream, nullptr, nullptr, nullptr, ws->err);
   if (s != CRT_OK) return s;
   return crt_quant_gemm(ws->codes, ldc, ws->s32, bits_a, L, M, out_kind, y, ldy, stream);
 }

@@ -23,6 +23,8 @@ extern template cudaError_t launch_any<4, true, 8>(const K1Args&, cudaStream_t, 
 extern template cudaError_t launch_any<16, true, 8>(const K1Args&, cudaStream_t, int64_t*);
 extern template cudaError_t launch_any<64, true, 8>(const K1Args&, cudaStream_t, int64_t*);
 extern template cudaError_t launch_any<256, true, 8>(const K1Args&, cudaStream_t, int64_t*);
+bool k1_team_eligible(const K1Args& a, bool f32, int bits) { return k1_team_ok(a, f32, bits); }
+
 template cudaError_t k1_dispatch<false, 4>(const K1Args&, int, cudaStream_t, int64_t*);
 template cudaError_t k1_exact_launch<false, 4>(const K1Args&, cudaStream_t);
 template cudaError_t k1_dispatch<false, 8>(const K1Args&, int, cudaStream_t, int64_t*);

@@ -46,4 +46,8 @@ K1Plan plan_k1(int64_t K, int64_t n0, int kind, bool identity_tail, bool f32, in
 cudaError_t launch_k1(const K1Args& a, const K1Plan& p, bool f32, int bits, cudaStream_t st,
                       int64_t* launches);
 
+// Would a fast-plan K1 with these arguments run the team kernel (which
+// skips the code stores when a.codes is null: amax-only launches)?
+bool k1_team_eligible(const K1Args& a, bool f32, int bits);
+
 }  // namespace crt

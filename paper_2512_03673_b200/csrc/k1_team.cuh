@@ -250,7 +250,9 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
     // ---- certified quantisation + pack + store from registers --------------
     uint8_t* crow = a.codes + row * a.ldc;
     int csum = 0;
-    if (!slow_row) {
+    if (!a.codes) {
+      // amax only (crt_rotated_row_absmax): no codes
+    } else if (!slow_row) {
       // inv = rk*QMAX/amax from an fp32 reciprocal (within 3 ulp of rk/s,
       // covered by the margin's slack); t = M + rint(y*inv) (low bits = code),
       // e = y*inv - rint(y*inv) certifies the decision (see k1_rolled)

@@ -137,7 +137,7 @@ class FluxStack:
                 ls, layer = u
                 x = self.inputs[(ls[0].m, ls[0].k)]
                 api.forward(x, layer, self.q, out="bf16", y=self.outputs[id(u)],
-                            workspace=self.ws)
+                            workspace=self.ws, check_finite=False)
             return
         main = torch.cuda.current_stream(self.device)
         self.side.wait_stream(main)
@@ -147,7 +147,7 @@ class FluxStack:
             txt = ".txt." in ls[0].name
             with torch.cuda.stream(self.side if txt else main):
                 api.forward(x, layer, self.q, out="bf16", y=self.outputs[id(u)],
-                            workspace=self.ws_side if txt else self.ws)
+                            workspace=self.ws_side if txt else self.ws, check_finite=False)
         main.wait_stream(self.side)
 
     def output_of(self, name: str) -> Optional[torch.Tensor]:

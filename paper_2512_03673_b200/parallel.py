@@ -26,6 +26,12 @@ The local compute is injectable (``local_forward``) so the host logic --
 shard ranges, the collective, the reassembly -- is testable on CPU with the
 ``gloo`` backend and the oracle standing in for the GPU kernels
 (tests/test_parallel.py).  The product path uses the CUDA kernels only.
+
+``TensorParallelLinear`` is the same two strategies through the C-ABI's
+tensor-parallel entry points (crt_tp_layer_prepare / crt_tp_forward): the
+NCCL collectives, the all-gather interleave and the row-parallel max / sum
+all-reduces run inside the library on one NCCL communicator
+(``NcclComm``), so a C++ host gets the identical sharded path.
 """
 from __future__ import annotations
 
@@ -185,3 +191,100 @@ def run_prompts(prompts: Sequence[torch.Tensor], fn: Callable[[torch.Tensor], to
     nranks = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     return [(i, fn(prompts[i])) for i in prompt_shard(len(prompts), rank, nranks)]
+
+
+# ---------------------------------------------------------------------------
+# The C-ABI tensor-parallel path (include/crt/convlinear4bit.h, crt_tp_*)
+# ---------------------------------------------------------------------------
+class NcclComm:
+    """An NCCL communicator for the library's tensor-parallel entry points,
+    one per rank on the current CUDA device.  The 128-byte unique id is made
+    on rank 0 and broadcast over the torch.distributed group (any backend)."""
+
+    def __init__(self, group: Optional[dist.ProcessGroup] = None):
+        import ctypes
+
+        from . import _abi
+        self._abi = _abi
+        lib = _abi.load()
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _abi.check(lib.crt_nccl_unique_id(uid))
+        if self.nranks > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _abi.check(lib.crt_nccl_comm_create(self.nranks, self.rank, uid, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._abi.load().crt_nccl_comm_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TensorParallelLinear:
+    """A ConvLinear4bit layer sharded over the ranks of an ``NcclComm``
+    through the C-ABI: ``mode="column"`` (output channels; x is the full
+    input, ``forward(x, gather=False)`` returns the [M, N/P] shard) or
+    ``mode="row"`` (input features; x is the rank's [M, K/P] columns, the
+    output the full [M, N] on every rank).  Bit-identical to one GPU."""
+
+    MODES = {"column": 1, "row": 2}
+
+    def __init__(self, w: torch.Tensor, bias: Optional[torch.Tensor], rotation, wq, aq,
+                 mode: str, comm: NcclComm, name: str = ""):
+        import ctypes
+
+        from . import _abi, api
+        if mode not in self.MODES:
+            raise ValueError("mode must be 'column' or 'row'")
+        self.mode, self.comm, self.aq, self.name = mode, comm, aq, name
+        self.nranks, self.rank = comm.nranks, comm.rank
+        N, K = w.shape
+        self.out_full, self.in_full = N, K
+        if bias is not None:
+            bias = bias.to(device=w.device, dtype=torch.float32).contiguous()
+        desc = _abi.LayerDescC(N, K, rotation.c(), wq.bits, api._dtype_code(w))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(w.device):
+            _abi.check(_abi.load().crt_tp_layer_prepare(
+                ctypes.byref(desc), api._ptr(w), w.stride(0), api._ptr(bias), self.MODES[mode],
+                comm.handle, api._stream(w), ctypes.byref(h)))
+        n_local = N // self.nranks if mode == "column" else N
+        k_local = K // self.nranks if mode == "row" else K
+        self.layer = api.PreparedLayer(h.value, n_local, k_local, rotation, wq, bias is not None,
+                                       name, w.device, (self.rank, self.nranks))
+
+    def forward(self, x: torch.Tensor, gather: bool = True, out: str = "bf16",
+                y: Optional[torch.Tensor] = None, workspace=None) -> torch.Tensor:
+        from . import _abi, api
+        M, K = x.shape
+        if K != self.layer.in_features:
+            raise api.ShapeError(f"input has {K} columns, the shard expects {self.layer.in_features}")
+        N = self.out_full if (self.mode == "row" or gather) else self.layer.out_features
+        if y is None:
+            y = torch.empty((M, N), dtype=api._OUT_DTYPE[out], device=x.device)
+        else:
+            api._check_out(y, M, N, out, self.layer.device)
+        ws = workspace or api._workspace_for(M, K, x.device)
+        _abi.check(_abi.load().crt_tp_forward(
+            self.layer.handle, api._ptr(x), api._dtype_code(x), M, x.stride(0), api._OUT[out],
+            api._ptr(y), y.stride(0), int(gather), ws.handle, self.comm.handle, api._stream(x)))
+        return y
+
+    __call__ = forward

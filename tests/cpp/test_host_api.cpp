@@ -102,7 +102,7 @@ static void gpu_tests() {
   cb::PreparedLayer L2 = cb::prepare_layer(w2, cb::DType::f32, N, K, K, b2, reg);
   cb::Workspace ws2(M, K);
   cb::forward(x2, cb::DType::f32, M, K, L2, cb::QuantSpec{4}, cb::Out::f32, y2, N, ws2);
-  cb::device_status();
+  ws2.status();
   std::vector<float> y(M * N);
   cudaMemcpy(y.data(), y2, y.size() * 4, cudaMemcpyDeviceToHost);
   for (int m = 0; m < M; ++m)
@@ -111,7 +111,20 @@ static void gpu_tests() {
   x[3] = NAN;
   cudaMemcpy(x2, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
   cb::forward(x2, cb::DType::f32, M, K, L2, cb::QuantSpec{4}, cb::Out::f32, y2, N, ws2);
-  EXPECT(throws<cb::InvalidValueError>([] { cb::device_status(); }));
+  EXPECT(throws<cb::InvalidValueError>([&] { ws2.status(); }));
+  ws2.status();  // cleared by the previous check
+  // non-finite weights: prepare_layer throws itself (compute_scales)
+  {
+    std::vector<float> wn(w);
+    wn[7] = INFINITY;
+    float* wn2;
+    cudaMalloc(&wn2, wn.size() * 4);
+    cudaMemcpy(wn2, wn.data(), wn.size() * 4, cudaMemcpyHostToDevice);
+    EXPECT(throws<cb::InvalidValueError>([&] {
+      cb::prepare_layer(wn2, cb::DType::f32, N, K, K, b2, reg);
+    }));
+    cudaFree(wn2);
+  }
   // int_gemm capacity precheck (pipeline.cpp:184-192) is host-side
   EXPECT(throws<cb::InvalidValueError>([&] {
     cb::forward(x2, cb::DType::f32, M, K, L2, cb::QuantSpec{5}, cb::Out::f32, y2, N, ws2);

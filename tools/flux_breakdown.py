@@ -19,7 +19,7 @@ for rep in range(2):
         x = st.inputs[(ls[0].m, ls[0].k)]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        api.forward(x, layer, st.q, out="bf16", y=st.outputs[id(u)], workspace=st.ws)
+        api.forward(x, layer, st.q, out="bf16", y=st.outputs[id(u)], workspace=st.ws, check_finite=False)
         b.record()
         b.synchronize()
         if rep == 1:
