@@ -55,9 +55,12 @@ def parse():
                     help="skip the per-config blocks (cfg1, cfg3 N0 sweep, cfg4 FLUX stack)")
     ap.add_argument("--cpu-stages", type=int, default=0, metavar="ROWS",
                     help=argparse.SUPPRESS)  # child process: staged CPU reference timing
-    ap.add_argument("--parallel", choices=["replica", "column"], default="replica",
-                    help="N>1: independent prompt replicas (weak scaling, default) or "
-                         "column-parallel fc1/fc2 with an NCCL all-gather (strong scaling)")
+    ap.add_argument("--parallel", choices=["replica", "column", "colrow"], default="replica",
+                    help="N>1: independent prompt replicas (weak scaling, default); column: "
+                         "fc1 and fc2 column-parallel, each output all-gathered (configs[4]); "
+                         "colrow: fc1 column-parallel WITHOUT a gather feeding fc2 "
+                         "row-parallel (one int32 SUM + M-double MAX all-reduce) -- both "
+                         "through the C-ABI tensor-parallel path (crt_tp_*, NCCL), strong scaling")
     return ap.parse_args()
 
 
@@ -479,15 +482,21 @@ def run_ours(args):
     w2 = torch.randn(D_MODEL, D_FF, device=dev, generator=gw).to(torch.bfloat16)
     b1 = torch.randn(D_FF, device=dev, generator=gw)
     b2 = torch.randn(D_MODEL, device=dev, generator=gw)
-    column = args.parallel == "column" and world > 1
-    if column:  # SURVEY.md 8e / configs[4]: output channels sharded, X replicated
-        fc1 = crt.prepare_layer_shard(w1, b1, spec, QuantSpec(4), rank, world, "fc1")
-        fc2 = crt.prepare_layer_shard(w2, b2, spec, QuantSpec(4), rank, world, "fc2")
+    column = args.parallel in ("column", "colrow")  # world 1: a 1-rank communicator
+    if column:
+        # SURVEY.md 8e / configs[4] through the C-ABI tensor-parallel path
+        from paper_2512_03673_b200.parallel import NcclComm, TensorParallelLinear
+        comm = NcclComm()
+        q4 = QuantSpec(4)
+        tp1 = TensorParallelLinear(w1, b1, spec, q4, q4, "column", comm, "fc1")
+        tp2 = TensorParallelLinear(w2, b2, spec, q4, q4,
+                                   "row" if args.parallel == "colrow" else "column", comm, "fc2")
+        fc1, fc2 = tp1.layer, tp2.layer
     else:
         fc1 = crt.prepare_layer(w1, b1, spec, QuantSpec(4), "fc1")
         fc2 = crt.prepare_layer(w2, b2, spec, QuantSpec(4), "fc2")
     del w1, w2
-    n1, n2 = fc1.out_features, fc2.out_features  # per-rank columns
+    n1, n2 = fc1.out_features, fc2.out_features  # per-rank columns (row: full N)
 
     # preallocated device buffers (no allocation in the timed region)
     # v3 (production forward): K1 writes one int8 per 4-bit code + per-row
@@ -507,11 +516,9 @@ def run_ours(args):
     y1 = torch.empty(M_TOK, D_FF, dtype=torch.bfloat16, device=dev)
     y2 = torch.empty(M_TOK, D_MODEL, dtype=torch.bfloat16, device=dev)
     if column:
-        from paper_2512_03673_b200.parallel import interleave_rank_major
+        ws_tp = crt.Workspace(M_TOK, D_FF, dev)
         y1s = torch.empty(M_TOK, n1, dtype=torch.bfloat16, device=dev)
-        y2s = torch.empty(M_TOK, n2, dtype=torch.bfloat16, device=dev)
-        g1 = torch.empty(world * M_TOK, n1, dtype=torch.bfloat16, device=dev)
-        g2 = torch.empty(world * M_TOK, n2, dtype=torch.bfloat16, device=dev)
+        x2s = torch.empty(M_TOK, D_FF // world, dtype=torch.bfloat16, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -538,28 +545,34 @@ def run_ours(args):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
     def step(record):
+        if column:  # C-ABI tensor-parallel forward of both layers
+            if record:
+                ev[0].record(stream)
+            if args.parallel == "colrow":
+                tp1(x, gather=False, y=y1s, workspace=ws_tp)   # [M, F/P]: fc2's input shard
+                if record:
+                    ev[2].record(stream)
+                tp2(y1s, y=y2, workspace=ws_tp)                # int32 all-reduce -> [M, D]
+            else:
+                tp1(x, gather=True, y=y1, workspace=ws_tp)     # all-gather + interleave
+                if record:
+                    ev[2].record(stream)
+                tp2(y1, gather=True, y=y2, workspace=ws_tp)
+            if record:
+                ev[4].record(stream)
+            return
         if record:
             ev[0].record(stream)
         k1(x, c1, s1, D_MODEL, ld1)
         if record:
             ev[1].record(stream)
-        if column:
-            k3(c1, ld1, s1, fc1, y1s, n1)
-            dist.all_gather_into_tensor(g1, y1s)
-            y1.copy_(interleave_rank_major(g1, world))
-        else:
-            k3(c1, ld1, s1, fc1, y1, D_FF)
+        k3(c1, ld1, s1, fc1, y1, D_FF)
         if record:
             ev[2].record(stream)
         k1(y1, c2, s2, D_FF, ld2)
         if record:
             ev[3].record(stream)
-        if column:
-            k3(c2, ld2, s2, fc2, y2s, n2)
-            dist.all_gather_into_tensor(g2, y2s)
-            y2.copy_(interleave_rank_major(g2, world))
-        else:
-            k3(c2, ld2, s2, fc2, y2, D_MODEL)
+        k3(c2, ld2, s2, fc2, y2, D_MODEL)
         if record:
             ev[4].record(stream)
 
@@ -593,11 +606,17 @@ def run_ours(args):
     launches = crt.launch_count() - launches0
     # Per-kernel breakdown (kernels_us, roofline): the same K steps again with
     # an event between every kernel (which serialises them).
-    seg = {"k1_fc1": [], "k3_fc1": [], "k1_fc2": [], "k3_fc2": [], "step": []}
+    seg = ({"fc1_tp": [], "fc2_tp": [], "step": []} if column else
+           {"k1_fc1": [], "k3_fc1": [], "k1_fc2": [], "k3_fc2": [], "step": []})
     for _ in range(args.steps):
         flush.zero_()
         step(True)
         ev[4].synchronize()
+        if column:
+            seg["fc1_tp"].append(ev[0].elapsed_time(ev[2]))
+            seg["fc2_tp"].append(ev[2].elapsed_time(ev[4]))
+            seg["step"].append(ev[0].elapsed_time(ev[4]))
+            continue
         seg["k1_fc1"].append(ev[0].elapsed_time(ev[1]))
         seg["k3_fc1"].append(ev[1].elapsed_time(ev[2]))
         seg["k1_fc2"].append(ev[2].elapsed_time(ev[3]))
@@ -620,7 +639,10 @@ def run_ours(args):
     value = (1 if column else world) * ops / (ms_step * 1e-3) / 1e12
 
     # roofline of the dominant kernel (K3), measured live on the launching stream
-    k3_us = (statistics.mean(seg["k3_fc1"]) + statistics.mean(seg["k3_fc2"])) / 2 * 1e3
+    if column:  # per-rank layer forward (K1 + K3 + collectives); no per-kernel split
+        k3_us = (statistics.mean(seg["fc1_tp"]) + statistics.mean(seg["fc2_tp"])) / 2 * 1e3
+    else:
+        k3_us = (statistics.mean(seg["k3_fc1"]) + statistics.mean(seg["k3_fc2"])) / 2 * 1e3
     k3_ops_per_launch = 2 * M_TOK * D_FF * D_MODEL // (world if column else 1)
     k3_tops = k3_ops_per_launch / (k3_us * 1e-6) / 1e12
     peaks = {}
@@ -634,7 +656,8 @@ def run_ours(args):
     # bf16 in + codes out + fp32 scale (+ int32 code sum for v3) per row
     k1_bytes = {k: M_TOK * kk * (2 + cpb) + (8 if v3 else 4) * M_TOK
                 for k, kk in (("fc1", D_MODEL), ("fc2", D_FF))}
-    k1_gbs = {k: k1_bytes[k] / (statistics.mean(seg[f"k1_{k}"]) * 1e-3) / 1e9 for k in k1_bytes}
+    k1_gbs = ({k: None for k in k1_bytes} if column else
+              {k: k1_bytes[k] / (statistics.mean(seg[f"k1_{k}"]) * 1e-3) / 1e9 for k in k1_bytes})
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "k3_traffic.json"))).get(
@@ -730,8 +753,10 @@ def run_ours(args):
                    "timing": configs["timing"]}
     else:
         k1_roof = {"bound": "hbm", "achieved": k1_gbs["fc2"], "peak": hbm, "unit": "GB/s",
-                   "frac": k1_gbs["fc2"] / hbm, "fc1_gbs": k1_gbs["fc1"],
-                   "bytes_per_launch": k1_bytes, "timing": "event-bracketed launches"}
+                   "frac": k1_gbs["fc2"] / hbm if k1_gbs["fc2"] else None,
+                   "fc1_gbs": k1_gbs["fc1"], "bytes_per_launch": k1_bytes,
+                   "timing": ("not split out in tensor-parallel runs" if column else
+                              "event-bracketed launches")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
@@ -741,11 +766,18 @@ def run_ours(args):
             "data": "synthetic (seeded gaussian bf16 activations, random-init weights)",
             "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
                        "n0": n0, "bits": "W4A4", "k3_path": args.path,
-                       "parallelism": (f"column-parallel x{world} + NCCL all-gather" if column else
-                                       f"prompt replicas x{world}" if world > 1 else "single"),
+                       "parallelism": (
+                           f"fc1 column-parallel (no gather) -> fc2 row-parallel (int32 SUM "
+                           f"all-reduce) x{world}, C-ABI crt_tp_* over NCCL"
+                           if column and args.parallel == "colrow" else
+                           f"column-parallel x{world} + NCCL all-gather, C-ABI crt_tp_*"
+                           if column else
+                           f"prompt replicas x{world}" if world > 1 else "single"),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "roofline": {"bound": "tensor",
-                         "kernel": ("k3_v3_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, weights "
+                         "kernel": ("per-rank tensor-parallel layer forward (K1 + K3 v3 + NCCL); "
+                                    "the ops are this rank's share" if column else
+                                    "k3_v3_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, weights "
                                     "expanded by tcgen05.cp decompression)") if v3 else
                                    "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
                          "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",

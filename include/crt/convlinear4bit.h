@@ -302,7 +302,7 @@ crt_status crt_tp_layer_prepare(const crt_layer_desc* desc, const void* w, int64
                                 crt_layer** out);
 /* Forward of a crt_tp_layer_prepare layer (see above); W4A4 / W8A8 as the
  * layer's bits.  Collective: every rank of `comm` must call it.  Scratch for
- * the gathered / reduced buffers is stream-ordered (cudaMallocAsync). */
+ * the gathered / reduced buffers is the workspace's (grown on first use). */
 crt_status crt_tp_forward(const crt_layer* layer, const void* x, int32_t x_dtype, int64_t M,
                           int64_t ldx, int32_t out_kind, void* y, int64_t ldy, int32_t gather,
                           crt_workspace* ws, void* comm, void* stream);

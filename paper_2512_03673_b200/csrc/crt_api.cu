@@ -546,6 +546,17 @@ crt_status crt_layer_export(const crt_layer* L, uint8_t* codes, int64_t ld_codes
 // ---------------------------------------------------------------------------
 }  // extern "C"
 
+void* crt_detail::workspace_tp_scratch(crt_workspace* ws, size_t bytes, cudaStream_t st) {
+  if (ws->tp_bytes >= bytes) return ws->tp_buf;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+  cudaFree(ws->tp_buf);
+  ws->tp_buf = nullptr;
+  ws->tp_bytes = 0;
+  if (cudaMalloc(&ws->tp_buf, bytes) != cudaSuccess) return nullptr;
+  ws->tp_bytes = bytes;
+  return ws->tp_buf;
+}
+
 crt_status crt_detail::quant_gemm_impl(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                                   const int32_t* a_sums, int32_t layout, int32_t bits_a,
                                   const crt_layer* L, int64_t M, int32_t out_kind, void* y,
@@ -622,18 +633,25 @@ __global__ void crt_dequant_kernel(const int32_t* __restrict__ acc, int64_t lda,
                                    int64_t N, const float* __restrict__ sa,
                                    const float* __restrict__ sw, const float* __restrict__ bias,
                                    int32_t out_kind, void* y, int64_t ldy) {
-  const int64_t total = M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / N, n = i - m * N;
-    const int32_t v = acc[m * lda + n];
-    if (out_kind == CRT_OUT_I32_ACC) {
-      reinterpret_cast<int32_t*>(y)[m * ldy + n] = v;
-      continue;
+  // one row per blockIdx.y, 8 consecutive columns per thread
+  const int64_t m = blockIdx.y;
+  const float s = sa[m];
+  const int32_t* ar = acc + m * lda;
+  for (int64_t n0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; n0 < N;
+       n0 += (int64_t)gridDim.x * blockDim.x * 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + j;
+      if (n >= N) break;
+      const int32_t v = ar[n];
+      if (out_kind == CRT_OUT_I32_ACC) {
+        reinterpret_cast<int32_t*>(y)[m * ldy + n] = v;
+        continue;
+      }
+      const float r = fmaf((float)v * s, sw[n], bias ? bias[n] : 0.f);
+      if (out_kind == CRT_OUT_BF16) reinterpret_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(r);
+      else reinterpret_cast<float*>(y)[m * ldy + n] = r;
     }
-    const float r = fmaf((float)v * sa[m], sw[n], bias ? bias[n] : 0.f);
-    if (out_kind == CRT_OUT_BF16) reinterpret_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(r);
-    else reinterpret_cast<float*>(y)[m * ldy + n] = r;
   }
 }
 
@@ -647,10 +665,13 @@ crt_status crt_dequant(const int32_t* acc, int64_t ld_acc, int64_t M, const floa
   if (M == 0 || N == 0) return CRT_OK;
   if (ld_acc < N || ldy < N) return fail(CRT_ERR_SHAPE, "ld < N");
   if (!acc || !y || !a_scales) return fail(CRT_ERR_INVALID_VALUE, "null buffer");
-  const int64_t total = M * N;
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
-  crt_dequant_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-      acc, ld_acc, M, N, a_scales, L->s32, L->bias, out_kind, y, ldy);
+  const int64_t bx = std::min<int64_t>((N + 2047) / 2048, 64);
+  for (int64_t m0 = 0; m0 < M; m0 += 65535) {  // gridDim.y limit
+    const int64_t mr = std::min<int64_t>(M - m0, 65535);
+    crt_dequant_kernel<<<dim3((unsigned)bx, (unsigned)mr), 256, 0, (cudaStream_t)stream>>>(
+        acc + m0 * ld_acc, ld_acc, mr, N, a_scales + m0, L->s32, L->bias, out_kind,
+        static_cast<char*>(y) + m0 * ldy * (out_kind == CRT_OUT_BF16 ? 2 : 4), ldy);
+  }
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "dequant launch");
@@ -684,6 +705,7 @@ crt_status crt_workspace_create(int64_t max_m, int64_t max_k, crt_workspace** ou
 
 crt_status crt_workspace_destroy(crt_workspace* w) {
   if (!w) return CRT_OK;
+  cudaFree(w->tp_buf);
   cudaFree(w->codes);
   cudaFree(w->s32);
   cudaFree(w->rowsum);

@@ -40,7 +40,15 @@ struct crt_workspace {
   float* s32;
   int32_t* rowsum;
   int* err;
+  void* tp_buf;      // crt_tp_forward scratch (gathered shards / row maxima +
+  size_t tp_bytes;   // int32 partials), grown on first use, owned here
 };
+
+namespace crt_detail {
+// ws->tp_buf with at least `bytes` (grows once: synchronises `st`, frees,
+// reallocates); null on failure.
+void* workspace_tp_scratch(crt_workspace* ws, size_t bytes, cudaStream_t st);
+}  // namespace crt_detail
 
 namespace crt_detail {
 

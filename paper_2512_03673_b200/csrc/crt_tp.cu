@@ -195,11 +195,12 @@ crt_status crt_tp_forward(const crt_layer* L, const void* x, int32_t x_dtype, in
     if (ldy < (gather ? N : Ns)) return fail(CRT_ERR_SHAPE, "ldy too small");
     if (M == 0) return CRT_OK;
     if (!gather || P == 1) return crt_forward(L, x, x_dtype, M, ldx, bits, out_kind, y, ldy, ws, stream);
-    void* local = nullptr;
-    void* gbuf = nullptr;
-    cudaError_t e = cudaMallocAsync(&local, (size_t)M * Ns * esz, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&gbuf, (size_t)P * M * Ns * esz, st);
-    if (e != cudaSuccess) return cuda_fail(e, "tp scratch");
+    const size_t lbytes = ((size_t)M * Ns * esz + 255) / 256 * 256;
+    char* buf = static_cast<char*>(workspace_tp_scratch(ws, lbytes + (size_t)P * M * Ns * esz, st));
+    if (!buf) return fail(CRT_ERR_CUDA, "tp scratch allocation failed");
+    void* local = buf;
+    void* gbuf = buf + lbytes;
+    cudaError_t e = cudaSuccess;
     s = crt_forward(L, x, x_dtype, M, ldx, bits, out_kind, local, Ns, ws, stream);
     if (s == CRT_OK) {
       const ncclDataType_t dt = out_kind == CRT_OUT_BF16 ? ncclBfloat16
@@ -220,8 +221,6 @@ crt_status crt_tp_forward(const crt_layer* L, const void* x, int32_t x_dtype, in
       e = cudaGetLastError();
       if (e != cudaSuccess) s = cuda_fail(e, "interleave launch");
     }
-    cudaFreeAsync(gbuf, st);
-    cudaFreeAsync(local, st);
     return s;
   }
 
@@ -234,11 +233,11 @@ crt_status crt_tp_forward(const crt_layer* L, const void* x, int32_t x_dtype, in
                                       "-deep accumulation can overflow int32");
   if (M == 0) return CRT_OK;
   if (M > ws->max_m || K > ws->max_k) return fail(CRT_ERR_SHAPE, "workspace too small");
-  double* amax = nullptr;
-  int32_t* acc = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&amax), (size_t)M * 8, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&acc), (size_t)M * N * 4, st);
-  if (e != cudaSuccess) return cuda_fail(e, "tp scratch");
+  const size_t abytes = ((size_t)M * 8 + 255) / 256 * 256;
+  char* buf = static_cast<char*>(workspace_tp_scratch(ws, abytes + (size_t)M * N * 4, st));
+  if (!buf) return fail(CRT_ERR_CUDA, "tp scratch allocation failed");
+  double* amax = reinterpret_cast<double*>(buf);
+  int32_t* acc = reinterpret_cast<int32_t*>(buf + abytes);
   // 1. exact per-row max of the shard (amax-only K1), 2. global max
   s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, bits, nullptr, 0, nullptr, nullptr, st,
              amax, nullptr, nullptr, ws->err);
@@ -261,8 +260,6 @@ crt_status crt_tp_forward(const crt_layer* L, const void* x, int32_t x_dtype, in
     if (r != ncclSuccess) s = nccl_fail(r, "ncclAllReduce(sum)");
   }
   if (s == CRT_OK) s = crt_dequant(acc, N, M, ws->s32, L, out_kind, y, ldy, stream);
-  cudaFreeAsync(acc, st);
-  cudaFreeAsync(amax, st);
   return s;
 }
 
