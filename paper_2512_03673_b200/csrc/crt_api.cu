@@ -738,7 +738,21 @@ crt_status crt_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64
   if (bits_a != 4 && bits_a != 8)  // pipeline.cpp:213-215
     return fail(CRT_ERR_INVALID_VALUE, "forward: activation bits must be 4 or 8");
   if (M > ws->max_m || K > ws->max_k) return fail(CRT_ERR_SHAPE, "workspace too small");
-  if (bits_a == 4 && L->desc.bits_w == 4 && L->tiles.codes_ob && M > 0) {
+  bool v3 = bits_a == 4 && L->desc.bits_w == 4 && L->tiles.codes_ob && M > 0;
+  if (v3) {  // the v3 GEMM's limits (K, TMA encode entry point); else the packed path
+    crt::K3Args probe{};
+    probe.a_codes = ws->codes;
+    probe.lda = (K + 15) / 16 * 16;
+    probe.a_layout = 1;
+    probe.a_sums = ws->rowsum;
+    probe.w = L->tiles;
+    probe.M = M;
+    probe.N = L->desc.out_features;
+    probe.K = K;
+    probe.bits = 4;
+    v3 = probe.N == 0 || crt::k3_v3_supported(probe);
+  }
+  if (v3) {
     // v3: int8-stored codes + code sums -> hardware-expanded weights GEMM
     const int64_t ldc = (K + 15) / 16 * 16;
     crt_status s = run_k1(x, x_dtype, M, K, ldx, &L->desc.rotation, 5, ws->codes, ldc, ws->s32,
