@@ -46,6 +46,14 @@ int* device_error_word() {
   return words[dev];
 }
 
+bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = getenv("CRT_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 crt_status fail(crt_status st, const std::string& msg) {
   g_err = msg;
   return st;
@@ -209,6 +217,7 @@ crt_status crt_rotate_quant(const void* x, int32_t x_dtype, int64_t M, int64_t K
                             const crt_rotation_spec* rot, int32_t bits, uint8_t* codes,
                             int64_t ld_codes, float* scales_f32, double* scales_f64,
                             void* stream) {
+  NvtxRange nvtx_("crt_rotate_quant (K1)");
   if (bits != 4 && bits != 8) return fail(CRT_ERR_INVALID_VALUE, "bits must be 4 or 8");
   return run_k1(x, x_dtype, M, K, ldx, rot, bits, codes, ld_codes, scales_f32, scales_f64,
                 (cudaStream_t)stream);
@@ -266,6 +275,7 @@ crt_status crt_device_status(void* stream, int32_t reset) {
 crt_status crt_detail::prepare_impl(const crt_layer_desc* d, const void* w, int64_t ldw,
                                const float* bias, int32_t rank, int32_t nranks,
                                cudaStream_t st, crt_layer** out) {
+  NvtxRange nvtx_("crt_layer_prepare (K2)");
   if (!d || !out) return fail(CRT_ERR_INVALID_VALUE, "null argument");
   *out = nullptr;
   if (d->bits_w != 4 && d->bits_w != 8) return fail(CRT_ERR_INVALID_VALUE, "bits_w must be 4 or 8");
@@ -606,6 +616,7 @@ extern "C" {
 crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                           int32_t bits_a, const crt_layer* L, int64_t M, int32_t out_kind,
                           void* y, int64_t ldy, void* stream) {
+  NvtxRange nvtx_("crt_quant_gemm (K3)");
   return quant_gemm_impl(a_codes, lda, a_scales, nullptr, 0, bits_a, L, M, out_kind, y, ldy,
                          stream);
 }
@@ -613,6 +624,7 @@ crt_status crt_quant_gemm(const uint8_t* a_codes, int64_t lda, const float* a_sc
 crt_status crt_rotate_quant_i8(const void* x, int32_t x_dtype, int64_t M, int64_t K, int64_t ldx,
                                const crt_rotation_spec* rot, uint8_t* codes, int64_t ld_codes,
                                float* scales_f32, int32_t* code_sums, void* stream) {
+  NvtxRange nvtx_("crt_rotate_quant_i8 (K1)");
   if (!code_sums) return fail(CRT_ERR_INVALID_VALUE, "null code_sums");
   return run_k1(x, x_dtype, M, K, ldx, rot, 5, codes, ld_codes, scales_f32, nullptr,
                 (cudaStream_t)stream, nullptr, code_sums);
@@ -621,6 +633,7 @@ crt_status crt_rotate_quant_i8(const void* x, int32_t x_dtype, int64_t M, int64_
 crt_status crt_quant_gemm_i8(const uint8_t* a_codes, int64_t lda, const float* a_scales,
                              const int32_t* code_sums, const crt_layer* L, int64_t M,
                              int32_t out_kind, void* y, int64_t ldy, void* stream) {
+  NvtxRange nvtx_("crt_quant_gemm_i8 (K3 v3)");
   if (!code_sums) return fail(CRT_ERR_INVALID_VALUE, "null code_sums");
   return quant_gemm_impl(a_codes, lda, a_scales, code_sums, 1, 4, L, M, out_kind, y, ldy, stream);
 }
@@ -657,6 +670,7 @@ __global__ void crt_dequant_kernel(const int32_t* __restrict__ acc, int64_t lda,
 
 crt_status crt_dequant(const int32_t* acc, int64_t ld_acc, int64_t M, const float* a_scales,
                        const crt_layer* L, int32_t out_kind, void* y, int64_t ldy, void* stream) {
+  NvtxRange nvtx_("crt_dequant");
   if (!L) return fail(CRT_ERR_INVALID_VALUE, "null layer");
   if (out_kind < CRT_OUT_BF16 || out_kind > CRT_OUT_I32_ACC)
     return fail(CRT_ERR_INVALID_VALUE, "bad out_kind");
@@ -733,6 +747,7 @@ crt_status crt_workspace_status(crt_workspace* w, void* stream, int32_t reset) {
 crt_status crt_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64_t M, int64_t ldx,
                        int32_t bits_a, int32_t out_kind, void* y, int64_t ldy, crt_workspace* ws,
                        void* stream) {
+  NvtxRange nvtx_("crt_forward (K1 + K3)");
   if (!L || !ws) return fail(CRT_ERR_INVALID_VALUE, "null layer / workspace");
   const int64_t K = L->desc.in_features;
   if (bits_a != 4 && bits_a != 8)  // pipeline.cpp:213-215

@@ -44,6 +44,23 @@ struct crt_workspace {
   size_t tp_bytes;   // int32 partials), grown on first use, owned here
 };
 
+// NVTX ranges around the C-ABI entry points (nvtx3 is header-only; the
+// ranges cost one branch unless CRT_NVTX=1 and a tool such as nsys or ncu
+// --nvtx is attached).  SURVEY.md 5 tracing.
+#include <nvtx3/nvToolsExt.h>
+namespace crt_detail {
+bool nvtx_on();
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+}  // namespace crt_detail
+
 namespace crt_detail {
 // ws->tp_buf with at least `bytes` (grows once: synchronises `st`, frees,
 // reallocates); null on failure.

@@ -173,6 +173,7 @@ crt_status crt_tp_layer_prepare(const crt_layer_desc* desc, const void* w, int64
 crt_status crt_tp_forward(const crt_layer* L, const void* x, int32_t x_dtype, int64_t M,
                           int64_t ldx, int32_t out_kind, void* y, int64_t ldy, int32_t gather,
                           crt_workspace* ws, void* comm, void* stream) {
+  NvtxRange nvtx_("crt_tp_forward");
   if (!L || !ws || !y) return fail(CRT_ERR_INVALID_VALUE, "null layer / workspace / output");
   if (L->tp_mode != CRT_TP_COLUMN && L->tp_mode != CRT_TP_ROW)
     return fail(CRT_ERR_INVALID_VALUE, "layer was not prepared with crt_tp_layer_prepare");
