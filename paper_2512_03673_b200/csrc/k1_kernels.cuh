@@ -18,6 +18,9 @@
 // is recomputed exactly the reference's way (sequential double sum in
 // ascending k, IEEE double division, nearbyint).  The output codes and f64
 // scales are therefore bit-identical to the reference for every input.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -1535,6 +1538,7 @@ cudaError_t launch_fast(const K1Args& a0, cudaStream_t st, int64_t* launches) {
 }  // namespace crt
 #include "k1_mma.cuh"
 #include "k1_team.cuh"
+#include "k1_tc.cuh"
 namespace crt {
 
 template <int N0, bool F32, int BITS>
@@ -1550,6 +1554,9 @@ cudaError_t launch_any(const K1Args& a, cudaStream_t st, int64_t* l) {
       const cudaError_t e = launch_mma<N0, BITS>(a, st, l);
       if (e != cudaErrorInvalidValue) return e;
     }
+  }
+  if constexpr (!F32 && (N0 == 4 || N0 == 16)) {
+    if (k1_tc_ok(a, BITS)) return launch_tc<N0, BITS>(a, st, l);
   }
   if (k1_team_ok(a, F32, BITS)) return launch_team<N0, F32, BITS>(a, st, l);
   static const bool fast = [] {
