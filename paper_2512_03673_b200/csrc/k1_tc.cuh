@@ -40,11 +40,12 @@
 
 namespace crt {
 
-constexpr int kK1TcStages = 4;
-constexpr int kK1TcThreads = 192;  // 4 compute warps + TMA warp + MMA warp
+constexpr int kK1TcStages = 8;
+constexpr int kK1TcThreads = 320;  // 8 compute warps (two warpgroups) + TMA warp + MMA warp
 constexpr int kK1TcUnit = 4096;    // bytes of one 128-group A tile
 
 struct K1TcArgs {
+  const void* x;         // M x K bf16, dense rows
   int64_t M, K;
   int32_t U, R;          // units per tile, rows per tile
   int64_t tiles;
@@ -95,9 +96,11 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity) {
+  // pure polling (mbarrier.test_wait): the pipeline's waits are on its
+  // critical path, and try_wait's suspend/wake-up costs more than the poll
   asm volatile(
       "{\n.reg .pred P1;\nTCW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra TCW_%=;\n}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
@@ -127,7 +130,7 @@ __device__ __noinline__ double tc_y_ref(const uint8_t* unit_smem, uint32_t grow,
   double acc = 0.0;
   for (int k = 0; k < N0; ++k) {
     const uint16_t b =
-        *reinterpret_cast<const uint16_t*>(unit_smem + tc_sw32(grow, (uint32_t)(e0 + k)));
+        *reinterpret_cast<const uint16_t*>(unit_smem + grow * 32u + (uint32_t)(e0 + k) * 2u);
     const double xv = (double)__uint_as_float((uint32_t)b << 16);
     acc = __dadd_rn(acc, __dmul_rn(xv, regular_negative((uint32_t)k, (uint32_t)j) ? -r : r));
   }
@@ -168,23 +171,23 @@ __device__ __noinline__ void tc_redecide(const uint8_t* us, uint32_t grow, uint3
   }
 }
 
-template <int N0, int BITS>
-__global__ void __launch_bounds__(kK1TcThreads, 4)
-    k1_tc_kernel(K1TcArgs a, const __grid_constant__ CUtensorMap xmap) {
+template <int N0, int BITS, int UH>
+__global__ void __launch_bounds__(kK1TcThreads, 1)
+    k1_tc_kernel(K1TcArgs a) {
   constexpr int QMAX = BITS == 8 ? 127 : 7;
-  constexpr int L = N0 == 4 ? 1 : 2;
+  constexpr int U = 2 * UH;  // units per tile; warpgroup h owns units [h*UH, (h+1)*UH)
   griddep_launch();
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   __shared__ __align__(1024) uint8_t hmat[16 * 32];  // B = H16 / blockdiag(H4), 32B swizzle
   __shared__ __align__(8) uint64_t full_bar[kK1TcStages], empty_bar[kK1TcStages];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base;
-  __shared__ uint32_t s_amax[4][2];
-  __shared__ double s_cmax[4][2];
-  __shared__ int s_sum[4][2];
+  __shared__ uint32_t s_amax[8][4];
+  __shared__ double s_cmax[8][4];
+  __shared__ int s_sum[8][4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int U = a.U, R = a.R, S = a.stages;
+  const int R = a.R, S = a.stages;
   const int64_t GR = a.K / 16;  // groups per row
   const uint32_t ring = smem_u32(tc_smem);
   const uint32_t fb = smem_u32(full_bar), eb = smem_u32(empty_bar);
@@ -193,23 +196,23 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 4);
+      mbar_init(&empty_bar[s], 8);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
+      mbar_init(&tempty_bar[b], 8);
     }
     mbar_init_fence();
   }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {  // B[n][k] = H[k][n]
     const int n = i >> 4, k = i & 15;
-    bool neg;
-    if (N0 == 16) neg = regular_negative((uint32_t)k, (uint32_t)n);
-    else neg = (k >> 2) == (n >> 2) ? regular_negative((uint32_t)(k & 3), (uint32_t)(n & 3)) : false;
-    const float v = (N0 == 4 && (k >> 2) != (n >> 2)) ? 0.f : (neg ? -1.f : 1.f);
-    *reinterpret_cast<__nv_bfloat16*>(hmat + tc_sw32((uint32_t)n, (uint32_t)k)) = __float2bfloat16(v);
+    const bool same = N0 == 16 || (k >> 2) == (n >> 2);
+    const bool neg = N0 == 16 ? regular_negative((uint32_t)k, (uint32_t)n)
+                              : regular_negative((uint32_t)(k & 3), (uint32_t)(n & 3));
+    *reinterpret_cast<__nv_bfloat16*>(hmat + tc_sw32((uint32_t)n, (uint32_t)k)) =
+        __float2bfloat16(same ? (neg ? -1.f : 1.f) : 0.f);
   }
-  if (warp == 5) {
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base)),
                  "r"(a.tmem_cols));
@@ -222,23 +225,25 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
   const uint32_t tmem = tmem_base;
   griddep_wait();  // the prologue above overlaps the predecessor's tail
 
-  const int64_t my_tiles = a.tiles > (int64_t)blockIdx.x ? (a.tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_tiles =
+      a.tiles > (int64_t)blockIdx.x ? (a.tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (warp == 4) {  // ---------------- TMA producer ----------------
+  if (warp == 8) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
       for (int64_t i = 0; i < my_tiles; ++i) {
         const int s = (int)(i % S);
         if (i >= S) tc_wait(eb + 8u * s, (uint32_t)((i / S - 1) & 1));
         const int64_t tile = blockIdx.x + i * gridDim.x;
-        mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(U * kK1TcUnit));
-        for (int u = 0; u < U; ++u)
-          tc_tma_2d(ring + (uint32_t)(s * U + u) * kK1TcUnit, &xmap, 0,
-                    (int)(tile * (int64_t)U * 128 + u * 128), fb + 8u * s);
+        // the tile's R whole rows are contiguous: one 1-D bulk copy (linear
+        // layout; the MMA reads it through a 32B-swizzle descriptor, see below)
+        const int64_t rows = std::min<int64_t>(R, a.M - tile * R);
+        const uint32_t bytes = (uint32_t)(rows * a.K * 2);
+        mbar_arrive_expect_tx(&full_bar[s], bytes);
+        bulk_g2s(tc_smem + (size_t)(s * U) * kK1TcUnit,
+                 reinterpret_cast<const char*>(a.x) + tile * R * a.K * 2, bytes, &full_bar[s]);
       }
     }
-    goto done;
-  }
-  if (warp == 5) {  // ---------------- MMA issuer ----------------
+  } else if (warp == 9) {  // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint64_t hdesc = tc_desc_sw32(smem_u32(hmat));
       const uint32_t idesc = tc_idesc_bf16(128, 16);
@@ -262,119 +267,163 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
             : "memory");
       }
     }
-    goto done;
-  }
-
-  {  // ---------------- compute warpgroup (warps 0-3) ----------------
-    const int t = threadIdx.x;  // TMEM lane of my group in every unit
+  } else {  // ---------------- compute: two warpgroups (warps 0-3, 4-7) ----------------
+    const int wg = warp >> 2;
+    const int t = (warp & 3) * 32 + lane;  // my TMEM lane = my group in every unit
+    // The A tiles are linear (32 B per group) but read through a 32B-swizzle
+    // descriptor, which swaps the two 16-byte halves of groups 4..7 of every
+    // 8: the MMA sees x[k ^ 8] there.  H16 (and blockdiag(H4)) commute with
+    // that half swap, so those lanes receive y[j ^ 8] in column j; the codes
+    // are put back in place when packed and the exact paths index the true
+    // elements.
+    const bool hswap = (t & 4) != 0;
     constexpr double rk = N0 == 4 ? 0.5 : 0.25;
-    constexpr double bound_rel = 64.0 * 1.1920928955078125e-7;  // B = bound_rel * A (see header)
+    constexpr double bound_rel = 64.0 * 1.1920928955078125e-7;  // B = bound_rel * A (header)
     constexpr float cand_scale = (float)((1.0 - 2.02 * bound_rel) * (1.0 - 2e-6));
     constexpr float q_thr =
         (float)(0.5 - (1.1 * bound_rel * QMAX + (QMAX + 4) * 9.5367431640625e-7 + 1e-9));
     constexpr float inv0 = (float)(rk * QMAX);
     const float mg = __uint_as_float(kMagic23 + (BITS == 4 ? 8u : 0u));
+    int urow[UH];  // row (within the tile) of my group in each of my units
+#pragma unroll
+    for (int uu = 0; uu < UH; ++uu) urow[uu] = (int)(((int64_t)(wg * UH + uu) * 128 + t) / GR);
     for (int64_t i = 0; i < my_tiles; ++i) {
       const int s = (int)(i % S), b = (int)(i & 1);
       const int64_t tile = blockIdx.x + i * gridDim.x;
       const int64_t row0 = tile * R;
       const uint8_t* stage = tc_smem + (size_t)(s * U) * kK1TcUnit;
-      const uint32_t tbuf = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * 16 * U);
+      const uint32_t tbuf = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(b * 16 * U);
       tc_wait(tfb + 8u * b, (uint32_t)((i >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // ---- the one TMEM read: my UH groups' 16 rotated values each -----------
+      float y[UH][16];
+#pragma unroll
+      for (int uu = 0; uu < UH; ++uu) {
+        uint32_t* r = reinterpret_cast<uint32_t*>(y[uu]);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+              "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+              "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(tbuf + (uint32_t)((wg * UH + uu) * 16)));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // TMEM buffer free for the next MMA as soon as every warp has its values
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc_arrive(teb + 8u * b);
 
-      // ---- pass 1: |y| max per row --------------------------------------
-      float lm[2] = {0.f, 0.f};
-      for (int u = 0; u < ((a.dbg & 4) ? 0 : U); ++u) {
-        float v[16];
-        tc_ld16(tbuf + (uint32_t)(u * 16), v);
+      // ---- |y| max per unit and per row ------------------------------------
+      float um[UH];
+#pragma unroll
+      for (int uu = 0; uu < UH; ++uu) {
         float m4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m4[k & 3] = max3_abs(v[2 * k], v[2 * k + 1], m4[k & 3]);
-        const float m = max_nan(max_nan(m4[0], m4[1]), max_nan(m4[2], m4[3]));
-        const int r = (int)((u * 128 + t) / GR);
-        lm[r] = max_nan(lm[r], m);
+        for (int k = 0; k < 8; ++k) m4[k & 3] = max3_abs(y[uu][2 * k], y[uu][2 * k + 1], m4[k & 3]);
+        um[uu] = max_nan(max_nan(m4[0], m4[1]), max_nan(m4[2], m4[3]));
       }
-      uint32_t wm[2];
-      float Aw[2];
-      for (int r = 0; r < R; ++r) {
-        wm[r] = __reduce_max_sync(0xffffffffu, __float_as_uint(lm[r]));
+      float lm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int uu = 0; uu < UH; ++uu)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (urow[uu] == r) lm[r] = max_nan(lm[r], um[uu]);
+      uint32_t wm[4];
+      float Aw[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        wm[r] = r < R ? __reduce_max_sync(0xffffffffu, __float_as_uint(lm[r])) : 0u;
         Aw[r] = __uint_as_float(wm[r]);
       }
-      // ---- pass 1b: this warp's row-max candidates, settled exactly --------
-      double cmax[2] = {0.0, 0.0};
+      // ---- this warp's row-max candidates, settled exactly ---------------------
+      double cmax[4] = {0.0, 0.0, 0.0, 0.0};
       if (!a.amax_in && !(a.dbg & 1)) {
-        bool slow[2];
-        float thr[2];
-        for (int r = 0; r < R; ++r) {
-          slow[r] = !(Aw[r] <= 3.0e38f);
-          thr[r] = Aw[r] * cand_scale;
-        }
-        for (int u = 0; u < U; ++u) {
-          const int r = (int)((u * 128 + t) / GR);
-          const bool need = slow[r] || (Aw[r] != 0.f && lm[r] >= thr[r]);
-          if (!__any_sync(0xffffffffu, need)) continue;
-          float v[16];
-          tc_ld16(tbuf + (uint32_t)(u * 16), v);  // all lanes (aligned ld)
-          if (!need) continue;
-          const uint8_t* us = stage + (size_t)u * kK1TcUnit;
+#pragma unroll
+        for (int uu = 0; uu < UH; ++uu) {
+          float aw = 0.f;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (urow[uu] == r) aw = Aw[r];
+          const bool slow = !(aw <= 3.0e38f);
+          const float thr = aw * cand_scale;
+          if (!(slow || (aw != 0.f && um[uu] >= thr))) continue;
           uint32_t m = 0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) m |= (slow[r] || fabsf(v[j]) >= thr[r] ? 1u : 0u) << j;
-          cmax[r] = fmax(cmax[r], tc_cands_exact<N0>(us, (uint32_t)t, m));
+          for (int j = 0; j < 16; ++j) m |= (slow || fabsf(y[uu][j]) >= thr ? 1u : 0u) << j;
+          if (hswap) m = ((m >> 8) | (m << 8)) & 0xFFFFu;
+          const double c = tc_cands_exact<N0>(stage + (size_t)(wg * UH + uu) * kK1TcUnit,
+                                              (uint32_t)t, m);
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (urow[uu] == r) cmax[r] = fmax(cmax[r], c);
         }
       }
-      for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (r >= R) break;
         const uint64_t bb = (uint64_t)__double_as_longlong(cmax[r]);
         const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(bb >> 32));
-        const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(bb >> 32) == hi ? (uint32_t)bb : 0u);
+        const uint32_t lo =
+            __reduce_max_sync(0xffffffffu, (uint32_t)(bb >> 32) == hi ? (uint32_t)bb : 0u);
         if (lane == 0) {
           s_amax[warp][r] = wm[r];
           s_cmax[warp][r] = __longlong_as_double((long long)(((uint64_t)hi << 32) | lo));
         }
       }
-      tc_named_sync(1, 128);
-      float A32[2];
-      double amax_ref[2];
-      bool invalid[2];
-      float inv[2];
-      for (int r = 0; r < R; ++r) {
+      tc_named_sync(1, 256);
+      float A32[4], inv[4];
+      double amax_ref[4];
+      bool invalid[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
         uint32_t am = 0;
         double cm = 0.0;
-        for (int w = 0; w < 4; ++w) {
-          am = max(am, s_amax[w][r]);
-          cm = fmax(cm, s_cmax[w][r]);
+        if (r < R) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            am = max(am, s_amax[w][r]);
+            cm = fmax(cm, s_cmax[w][r]);
+          }
         }
         A32[r] = __uint_as_float(am);
         const int64_t row = row0 + r;
-        amax_ref[r] = a.amax_in ? (row < a.M ? a.amax_in[row] : 0.0) : cm;
-        if (!a.amax_in && !(A32[r] <= 3.0e38f)) amax_ref[r] = cm;  // exact loop's max (+inf if bad)
+        amax_ref[r] = a.amax_in ? (r < R && row < a.M ? a.amax_in[row] : 0.0) : cm;
         invalid[r] = !isfinite(amax_ref[r]);
         inv[r] = amax_ref[r] == 0.0 ? (float)rk : inv0 * __frcp_rn((float)amax_ref[r]);
       }
-      // ---- pass 2: certified quantisation + pack + store --------------------
-      int csum[2] = {0, 0};
+      // ---- certified quantisation + pack + store from registers ----------------
+      int csum[4] = {0, 0, 0, 0};
       if (a.codes && !(a.dbg & 2)) {
-        for (int u = 0; u < U; ++u) {
-          const int64_t g = (int64_t)u * 128 + t;  // group within the tile
-          const int r = (int)(g / GR);
+#pragma unroll
+        for (int uu = 0; uu < UH; ++uu) {
+          const int r = urow[uu];
+          float ir = 0.f, a32 = 0.f;
+          bool inval = false;
+          double aref = 0.0;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (r == rr) {
+              ir = inv[rr];
+              a32 = A32[rr];
+              inval = invalid[rr];
+              aref = amax_ref[rr];
+            }
           const int64_t row = row0 + r;
-          float v[16];
-          tc_ld16(tbuf + (uint32_t)(u * 16), v);
           if (row >= a.M) continue;
-          const int64_t gc = g - (int64_t)r * GR;  // group (= 16-element chunk) within the row
+          const int64_t gc = (int64_t)(wg * UH + uu) * 128 + t - (int64_t)r * GR;
           uint8_t* crow = a.codes + row * a.ldc;
-          const uint8_t* us = stage + (size_t)u * kK1TcUnit;
+          const uint8_t* us = stage + (size_t)(wg * UH + uu) * kK1TcUnit;
           uint32_t tb[16];
-          const bool exact_all = !(A32[r] <= 3.0e38f);  // slow row: every element exactly
-          uint32_t fm = exact_all ? 0xFFFFu : 0u;         // elements decided exactly
+          const bool exact_all = !(a32 <= 3.0e38f);  // slow row: every element exactly
+          uint32_t fm = exact_all ? 0xFFFFu : 0u;
           {
-            const float2 iv = make_float2(inv[r], inv[r]);
+            const float2 iv = make_float2(ir, ir);
             const float2 cc = make_float2(mg, mg);
             float em = 0.f;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              const float2 yv = make_float2(v[2 * k], v[2 * k + 1]);
+              const float2 yv = make_float2(y[uu][2 * k], y[uu][2 * k + 1]);
               const float2 tt = __ffma2_rn(yv, iv, cc);
               const float2 nr = __ffma2_rn(tt, make_float2(-1.f, -1.f), cc);
               const float2 e = __ffma2_rn(yv, iv, nr);
@@ -385,7 +434,7 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
             if (!exact_all && !(em <= q_thr)) {  // rare: near-ties
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                const float ex = fmaf(v[j], inv[r], mg - fmaf(v[j], inv[r], mg));
+                const float ex = fmaf(y[uu][j], ir, mg - fmaf(y[uu][j], ir, mg));
                 fm |= (fabsf(ex) <= q_thr ? 0u : 1u) << j;
               }
             }
@@ -400,7 +449,7 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
                               0x5410) ^ 0x88888888u;
             o.y = __byte_perm(__byte_perm(by[4], by[5], 0x0040), __byte_perm(by[6], by[7], 0x0040),
                               0x5410) ^ 0x88888888u;
-            *reinterpret_cast<uint2*>(crow + gc * 8) = o;
+            *reinterpret_cast<uint2*>(crow + gc * 8) = hswap ? make_uint2(o.y, o.x) : o;
           } else {
             uint32_t wd[4];
 #pragma unroll
@@ -409,53 +458,65 @@ __global__ void __launch_bounds__(kK1TcThreads, 4)
                                   __byte_perm(tb[4 * q + 2], tb[4 * q + 3], 0x0040), 0x5410);
               if constexpr (BITS == 5) cs = __dp4a((int)wd[q], 0x01010101, cs);
             }
-            *reinterpret_cast<uint4*>(crow + gc * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            *reinterpret_cast<uint4*>(crow + gc * 16) =
+                hswap ? make_uint4(wd[2], wd[3], wd[0], wd[1]) : make_uint4(wd[0], wd[1], wd[2], wd[3]);
           }
+          if (hswap) fm = ((fm >> 8) | (fm << 8)) & 0xFFFFu;  // true element positions
           if (fm) {  // the owner rewrites the flagged codes it just stored
-            const double sr = invalid[r] ? 0.0
-                              : (amax_ref[r] == 0.0 ? 1.0 : amax_ref[r] / (double)QMAX);
+            const double sr = inval ? 0.0 : (aref == 0.0 ? 1.0 : aref / (double)QMAX);
             tc_redecide<N0, BITS>(us, (uint32_t)t, fm, sr, crow, gc);
             if constexpr (BITS == 5) {
               const uint4 w4 = *reinterpret_cast<const uint4*>(crow + gc * 16);
-              cs = __dp4a((int)w4.x, 0x01010101, __dp4a((int)w4.y, 0x01010101,
-                   __dp4a((int)w4.z, 0x01010101, __dp4a((int)w4.w, 0x01010101, 0))));
+              cs = __dp4a((int)w4.x, 0x01010101,
+                          __dp4a((int)w4.y, 0x01010101,
+                                 __dp4a((int)w4.z, 0x01010101, __dp4a((int)w4.w, 0x01010101, 0))));
             }
           }
-          csum[r] += cs;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (r == rr) csum[rr] += cs;
         }
       }
-      // ---- row bookkeeping, release the stage and the TMEM buffer ----------
+      // ---- row bookkeeping; the stage is free once every warp is past it ----
       if constexpr (BITS == 5) {
-        for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r >= R) break;
           const int ws = __reduce_add_sync(0xffffffffu, csum[r]);
           if (lane == 0) s_sum[warp][r] = ws;
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
-        tc_arrive(teb + 8u * b);
-        tc_arrive(eb + 8u * s);
-      }
-      tc_named_sync(1, 128);
-      if (t < R) {
-        const int r = t;
+      if (lane == 0) tc_arrive(eb + 8u * s);
+      tc_named_sync(1, 256);
+      if (threadIdx.x < R) {
+        const int r = threadIdx.x;
         const int64_t row = row0 + r;
         if (row < a.M) {
-          const double sc = invalid[r] ? 1.0 : (amax_ref[r] == 0.0 ? 1.0 : amax_ref[r] / (double)QMAX);
-          if (invalid[r]) flag_invalid_value(a.err);
+          double ar = 0.0;
+          bool iv = false;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (r == rr) {
+              ar = amax_ref[rr];
+              iv = invalid[rr];
+            }
+          const double sc = iv ? 1.0 : (ar == 0.0 ? 1.0 : ar / (double)QMAX);
+          if (iv) flag_invalid_value(a.err);
           if (a.s32) a.s32[row] = (float)sc;
           if (a.s64) a.s64[row] = sc;
-          if (a.amax) a.amax[row] = amax_ref[r];
-          if (BITS == 5 && a.rowsum && a.codes)
-            a.rowsum[row] = s_sum[0][r] + s_sum[1][r] + s_sum[2][r] + s_sum[3][r];
+          if (a.amax) a.amax[row] = ar;
+          if (BITS == 5 && a.rowsum && a.codes) {
+            int sum = 0;
+            for (int w = 0; w < 8; ++w) sum += s_sum[w][r];
+            a.rowsum[row] = sum;
+          }
         }
       }
     }
   }
-done:
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+  if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                                "r"(a.tmem_cols));
 }
 
@@ -487,20 +548,29 @@ inline bool k1_tc_ok(const K1Args& a, int bits) {
   }();
   if (!on || a.kind != kRotRegular || (a.group != 4 && a.group != 16)) return false;
   if (a.rot_cols != a.K || a.K % 1024 != 0 || a.K > 16384 || a.K <= 0 || a.M <= 0) return false;
+  {  // tile geometry: R rows = U units, U even and <= 6, R <= 4
+    int R = 1;
+    while ((R * a.K) % 4096 != 0) ++R;
+    const int64_t U = R * a.K / 2048;
+    if (R > 4 || U > 6 || U < 2) return false;
+  }
   if (a.ldx != a.K || (uintptr_t)a.x % 16) return false;
   if (a.M * (a.K / 16) >= ((int64_t)1 << 31)) return false;
   if (a.rowsum && bits != 5) return false;
   if (a.codes && ((uintptr_t)a.codes % 16 || a.ldc % 16)) return false;
-  return k1_tc_encode_fn() != nullptr;
+  return true;
 }
 
 template <int N0, int BITS>
 cudaError_t launch_tc(const K1Args& a, cudaStream_t st, int64_t* launches) {
   const int num_sms = device_sm_count();
   K1TcArgs t{};
+  t.x = a.x;
   t.M = a.M;
   t.K = a.K;
-  t.R = a.K % 2048 == 0 ? 1 : 2;
+  // a tile is R whole rows = U units of 128 groups, U = 2*UH (two warpgroups)
+  t.R = 1;
+  while ((t.R * a.K) % 4096 != 0) ++t.R;  // R*K/2048 even
   t.U = (int32_t)(t.R * a.K / 2048);
   t.tiles = (a.M + t.R - 1) / t.R;
   uint32_t cols = 32;
@@ -518,53 +588,37 @@ cudaError_t launch_tc(const K1Args& a, cudaStream_t st, int64_t* launches) {
     const char* e = getenv("CRT_K1_TC_DBG");
     t.dbg = e ? atoi(e) : 0;
   }
+  auto kern = t.U == 2 ? k1_tc_kernel<N0, BITS, 1>
+              : t.U == 4 ? k1_tc_kernel<N0, BITS, 2> : k1_tc_kernel<N0, BITS, 3>;
+  // CTAs per SM: TMEM (512 columns), registers; then the deepest ring that
+  // fits next to them (the occupancy API reports 1 for this kernel although
+  // several ~50 KB CTAs fit; persistent CTAs over disjoint tile lists, so any
+  // residency is correct)
   int per_sm = (int)(512 / cols);
-  const size_t stage_bytes = (size_t)t.U * kK1TcUnit;
-  int S = kK1TcStages;
-  while (S > 2 && (size_t)per_sm * S * stage_bytes > (size_t)200 * 1024) --S;
-  while (per_sm > 1 && (size_t)per_sm * S * stage_bytes > (size_t)200 * 1024) --per_sm;
-  t.stages = S;
-  const size_t smem = (size_t)S * stage_bytes;
-  CUtensorMap map;
-  {
-    cuuint64_t dims[2] = {16, (cuuint64_t)(a.M * (a.K / 16))};
-    cuuint64_t strides[1] = {32};
-    cuuint32_t box[2] = {16, 128};
-    cuuint32_t es[2] = {1, 1};
-    if (k1_tc_encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.x), dims,
-                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
-  }
-  auto kern = k1_tc_kernel<N0, BITS>;
-  {
-    static SmemAttr attr;
-    const cudaError_t e = ensure_dyn_smem(kern, smem, attr, true);
-    if (e != cudaSuccess) return e;
-  }
-  int occ = 0;
-  const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK1TcThreads, smem);
-  static const bool dbg = getenv("CRT_K1_TC_DEBUG") != nullptr;
-  if (dbg)
-    fprintf(stderr, "[k1_tc] U=%d R=%d tiles=%lld cols=%u S=%d smem=%zu per_sm(tmem/smem)=%d occ=%d (%s)\n",
-            t.U, t.R, (long long)t.tiles, cols, S, smem, per_sm, occ, cudaGetErrorString(oe));
-  // the occupancy API reports 1 for this kernel although 4 CTAs of ~50 KB
-  // fit the 228 KB carveout (measured: 4 co-resident CTAs run); the CTAs
-  // per SM are bounded by TMEM (512 columns), shared memory and registers
-  // directly (persistent CTAs over disjoint tile lists: any residency is
-  // correct, only the speed changes)
   {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);
-    const int by_regs = fa.numRegs > 0 ? 65536 / (fa.numRegs * kK1TcThreads) : per_sm;
-    const int by_smem = (int)((size_t)227 * 1024 / (smem + fa.sharedSizeBytes + 1024));
-    per_sm = std::min(per_sm, std::min(by_regs, by_smem));
+    if (fa.numRegs > 0) per_sm = std::min(per_sm, 65536 / (fa.numRegs * kK1TcThreads));
     if (per_sm < 1) per_sm = 1;
   }
+  const size_t stage_bytes = (size_t)t.U * kK1TcUnit;
+  int S = kK1TcStages;
+  while (S > 2 && (size_t)per_sm * (S * stage_bytes + 4096) > (size_t)220 * 1024) --S;
+  while (per_sm > 1 && (size_t)per_sm * (S * stage_bytes + 4096) > (size_t)220 * 1024) --per_sm;
+  t.stages = S;
+  const size_t smem = (size_t)S * stage_bytes;
+  {
+    static SmemAttr attr[4];
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[t.U / 2], true);
+    if (e != cudaSuccess) return e;
+  }
+  static const bool dbg = getenv("CRT_K1_TC_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[k1_tc] U=%d R=%d tiles=%lld cols=%u S=%d smem=%zu per_sm=%d\n", t.U, t.R,
+            (long long)t.tiles, cols, S, smem, per_sm);
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > t.tiles) grid = t.tiles;
-  const cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(kK1TcThreads), smem, st, t, map);
+  const cudaError_t le = launch_pdl(kern, dim3((unsigned)grid), dim3(kK1TcThreads), smem, st, t);
   ++*launches;
   return le;
 }
