@@ -1,5 +1,6 @@
-"""Opt-in kernel paths stay bit-exact: the tensor-core K1 (CRT_K1_MMA=1), the
-register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
+"""Opt-in kernel paths stay bit-exact: the mma.sync K1 (CRT_K1_MMA=1), the
+tcgen05 tensor-core K1 (CRT_K1_TC=1), the round-1 rolled K1 (CRT_K1_TEAM=0),
+the register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
 (CRT_K3_V1=1), the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-lane
 store epilogue (CRT_K3_DIRECT_STORES=1), each -- and the defaults -- in a fresh
 process."""
@@ -13,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K3_V1": "1"},
+@pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K1_TC": "1"},
+                                 {"CRT_K1_TEAM": "0"}, {"CRT_K3_V1": "1"},
                                  {"CRT_K3_W8_TS": "1"}, {"CRT_K3_DIRECT_STORES": "1"},
                                  {"CRT_K3_NO_FDQ": "1"}])
 def test_opt_in_paths_bit_exact(env):
