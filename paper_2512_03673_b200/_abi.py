@@ -93,6 +93,7 @@ _SIGS = {
     "crt_last_error": (ctypes.c_char_p, []),
     "crt_launch_count": (_I64, []),
     "crt_debug_k1_trace": (None, [_P]),
+    "crt_debug_k3_trace": (None, [_P]),
     "crt_regular_hadamard": (_I32, [_I32, _P]),
     "crt_sylvester_hadamard": (_I32, [_I32, _P]),
     "crt_rotate_quant": (_I32, [_P, _I32, _I64, _I64, _I64, ctypes.POINTER(RotationSpecC), _I32,

@@ -183,6 +183,7 @@ int32_t crt_abi_version(void) { return CRT_ABI_VERSION; }
 const char* crt_last_error(void) { return g_err.c_str(); }
 int64_t crt_launch_count(void) { return g_launches.load(); }
 void crt_debug_k1_trace(void* buf) { crt::set_k1_trace(static_cast<unsigned long long*>(buf)); }
+void crt_debug_k3_trace(void* buf) { crt::set_k3_trace(static_cast<unsigned long long*>(buf)); }
 
 // hadamard.cpp:91-106 / :108-126.  H_{4^L}[r][c] = prod_s H4[r_s][c_s]; the
 // Kronecker rule puts the right factor on the least significant base-4

@@ -63,6 +63,10 @@ bool k3_v2_supported(const K3Args& a);
 // weights into TMEM, int8 activation codes as the smem operand (k3_gemm_v3.cu).
 bool k3_v3_supported(const K3Args& a);
 cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
+// Dev aid (crt_debug_k3_trace): when set, k3_v3 records clock64 stamps of
+// pair 0's leader CTA (9 rows x 4096, see k3_gemm_v3.cu); null = off.
+void set_k3_trace(unsigned long long* buf);
+unsigned long long* k3_trace();
 cudaError_t k3_v2_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 
 }  // namespace crt

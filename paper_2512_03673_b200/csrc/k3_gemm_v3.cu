@@ -17,11 +17,12 @@
 //     acc = (acc' - 32*S_a[m]) >> 2 exactly (|acc'| < 2^31 for K <= 1,277,000).
 // Pair tile: 256 channels (128 per CTA, A from its own TMEM) x 192 tokens
 // (96 token rows of B per CTA).  Persistent over tiles; warp roles: 0 TMA
-// producer, 1 MMA issuer, 3 decompress issuer (a separate tcgen05 issuing
-// thread, so the smem->TMEM expansion runs beside the MMAs instead of in
-// their in-order queue: fc2 2105 -> 2693 TOPS), 4..11 epilogue.  The
-// accumulators are double buffered so the epilogue (TMEM -> dequant ->
-// direct coalesced stores, lane = channel) overlaps the next tile's MMAs.
+// producer, 1 and 2 MMA issuers (alternate K stages, each expanding its
+// stage's A with tcgen05.cp right before its MMAs; two issuers because one
+// thread's mbarrier wait after its commits drains its MMA pipeline -- see
+// the issuer section), 4..11 epilogue (warp 3 idle).  The accumulators are double
+// buffered so the epilogue (TMEM -> dequant -> stores, lane = channel)
+// overlaps the next tile's MMAs.
 // TMEM per CTA (512 columns): acc0 [0,192), A slots 0,1 [192,256), acc1
 // [256,448), A slots 2,3 [448,512); one slot = one 128-code K block.
 #include <cuda.h>
@@ -30,6 +31,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <atomic>
 
 #include "common.cuh"
 #include "k3_gemm.h"
@@ -40,8 +43,8 @@ namespace {
 constexpr int V3_BM = 128;         // channels per CTA (pair: 256)
 constexpr int V3_BT = 192;         // tokens per pair tile (measured: 160 and 224 both ~20% slower)
 constexpr int V3_BTH = V3_BT / 2;  // token rows of B per CTA
-constexpr int V3_PS = 7;           // smem stages
-constexpr int V3_THREADS = 384;
+constexpr int V3_PS = 8;           // smem stages (8 x 28 KB: the epilogue stages nothing)
+constexpr int V3_THREADS = 384;  // 12 warps: producer, 2 MMA issuers, (idle), 8 epilogue
 constexpr int V3_A_STAGE = V3_BM * 128;  // 16 KB: 128 rows x (8 x 16 B padded units)
 constexpr int V3_B_STAGE = V3_BTH * 128; // 12 KB int8
 // TMEM (512 columns): two V3_BT-column accumulators at 0 and 256, the rest of
@@ -61,11 +64,10 @@ struct V3Smem {
   uint64_t empty[V3_PS];  // both: MMA commit multicast
   uint64_t acc_full[2];   // both: MMA commit multicast
   uint64_t acc_empty[2];  // leader: 8 epilogue warps x 2 CTAs
-  uint64_t dec_full[V3_SLOTS];   // leader: decompress warp's commit (A slot expanded)
-  uint64_t dec_empty[V3_SLOTS];  // leader: MMA commit (A slot consumed)
+  uint64_t dec_empty[V3_SLOTS];  // leader: MMA commit (A slot consumed by its issuer)
   uint32_t tmem_base;
-  alignas(16) float sa[2][V3_BT];  // per-token activation scale of the tile (ld.shared.v4)
-  alignas(16) int sums[2][V3_BT];  // per-token code sums, x32
+  alignas(16) float sa[V3_BT];  // per-token activation scale of the tile (ld.shared.v4)
+  alignas(16) int sums[V3_BT];  // per-token code-sum offsets of the tile
 };
 
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
@@ -199,6 +201,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// zero 32 lanes x 32 columns of TMEM (the accumulator chunk just read), so
+// the next tile's MMAs can all accumulate (two issuers, no zeroing MMA)
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
 
 // 16-byte shared-memory broadcast load (every lane reads the same address).
 __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
@@ -230,43 +243,29 @@ struct V3Args {
   void* y;
   int64_t ldy;
   int32_t w8_ss;     // W8A8: A straight from shared memory (no TMEM copy)
-  int32_t fdq;       // magic-number fp32x2 dequant in the TMA-store epilogue
-  int32_t y_tma;     // bf16 output through shared-memory staging + TMA bulk stores
+  int32_t fdq;       // magic-number fp32x2 dequant (bf16 output)
+  int32_t dbg_skip_epi;       // dev aid (CRT_K3_DBG_SKIP_EPI=1): TMEM reads only, no dequant/stores
+  unsigned long long* trace;  // dev aid (crt_debug_k3_trace): pair 0's leader clock64 stamps
 };
-
-// Epilogue output staging: one 32-token x 32-channel bf16 box (2 KB) per
-// epilogue warp, written with st.shared and stored by one TMA bulk tensor
-// store (the async proxy writes the 64 B rows; no per-lane global stores).
-constexpr int V3_YSTG = 2048;
-__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+// trace layout: 9 rows x kK3TraceN; per stage: row 0 producer issue, row 3
+// MMA issue (stage landed, slot free), row 7 the issuer before its waits,
+// row 8 after its copies, MMAs and commits; per tile: row 4 first issuer's
+// tile start, 5 epilogue sees acc_full, 6 epilogue done; rows 1-2 unused
+constexpr int kK3TraceN = 4096;
+__device__ __forceinline__ void k3_stamp(unsigned long long* tr, int row, int i) {
+  if (tr && i < kK3TraceN) tr[row * kK3TraceN + i] = clock64();
 }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t saddr, int x, int y) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   map),
-               "r"(x), "r"(y), "r"(saddr)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // W8 = false: W4A4 (offset-binary int4 weights, hardware expansion);
 // W8 = true: W8A8 (int8 weights and activations).
 template <bool W8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     k3_v3_kernel(const __grid_constant__ CUtensorMap map_w,
-                 const __grid_constant__ CUtensorMap map_x,
-                 const __grid_constant__ CUtensorMap map_y, V3Args a) {
+                 const __grid_constant__ CUtensorMap map_x, V3Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = smem;                                        // V3_PS x (A 16 KB | B 12 KB)
   V3Smem* ss = reinterpret_cast<V3Smem*>(smem + V3_PS * V3_STAGE);
-  uint8_t* ystg = smem + V3_PS * V3_STAGE + ((sizeof(V3Smem) + 127) & ~(size_t)127);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -276,6 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
   const int pair = blockIdx.x >> 1;
   const int ntiles = a.ttiles * a.ctiles;
   const int KB = (int)((a.K + 127) / 128);
+  unsigned long long* const tr = (a.trace && pair == 0 && leader) ? a.trace : nullptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < V3_PS; ++s) {
@@ -283,11 +283,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
       mbar_init(&ss->empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&ss->acc_full[b], 1);
+      mbar_init(&ss->acc_full[b], 2);  // one commit per MMA issuer
       mbar_init(&ss->acc_empty[b], 16);
     }
     for (int b = 0; b < V3_SLOTS; ++b) {
-      mbar_init(&ss->dec_full[b], 1);
       mbar_init(&ss->dec_empty[b], 1);
     }
     mbar_init_fence();
@@ -307,7 +306,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
   if (warp == 0 && lane == 0) {  // kernel parameters, not predecessor output
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
-    if (a.y_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_y) : "memory");
   }
   griddep_launch();
   griddep_wait();
@@ -316,14 +314,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     // ===== TMA producer (both CTAs; completions land on the leader) ========
     if (lane == 0) {
       const uint32_t full0 = mapa(smem_u32(&ss->full[0]), 0);
-      int s = 0;
+      int s = 0, g = 0;
       uint32_t ph = 0;
       for (int t = pair; t < ntiles; t += npairs) {
         const int tt = t % a.ttiles, ct = t / a.ttiles;
         const int n0 = ct * 2 * V3_BM + (int)rank * V3_BM;   // this CTA's channels
         const int m0 = tt * V3_BT + (int)rank * V3_BTH;      // this CTA's token rows
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = 0; kb < KB; ++kb, ++g) {
           mbar_wait(&ss->empty[s], ph ^ 1);
+          k3_stamp(tr, 0, g);
           if (leader) mbar_arrive_expect_tx(&ss->full[s], 2 * (W8 ? V3_STAGE_TX_W8 : V3_STAGE_TX));
           else arrive_cluster(full0 + s * 8);
           uint8_t* st = stg + s * V3_STAGE;
@@ -336,19 +335,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer (leader) ===============================================
+  } else if (warp == 1 || warp == 2) {
+    // ===== MMA issuers (leader): two threads, alternate stages ===============
+    // An MMA-issuing thread that touches shared memory (an mbarrier wait)
+    // while one of its tcgen05.commit arrivals is pending stalls until its
+    // MMA pipeline drains: one issuer with K3's per-stage wait + commits
+    // keeps the tensor pipe ~70% busy (tools/probes/i8_peak_probe.cu:
+    // 137.5 cycles per M256xN192xK32 MMA instead of 96).  The drain is per
+    // issuing thread, so two issuers (warps 1 and 2) taking alternate stages
+    // keep it full (96.0) -- they accumulate into the same TMEM accumulator,
+    // exact for integers in any order (probe: 0 wrong of 3.6M elements).
+    // All MMAs accumulate: the epilogue zeroes each accumulator after
+    // reading it (and both once at start), so neither issuer orders against
+    // the other's first MMA of a tile.  acc_full takes one commit from each.
+    // Each issuer also expands the A operand of its stage (tcgen05.cp from
+    // the padded smem stage into a TMEM slot) right before the stage's
+    // MMAs: cp -> mma from one thread execute in order.  Measured and
+    // rejected: one separate expansion thread (its own waits drain its
+    // copies: ~580 cycles per stage), two expansion threads (the copies queue
+    // behind the MMAs already issued, so the issuers wait ~900 cycles for
+    // them: 2757 vs 2819 TOPS at fc1), and expanding two stages ahead inside
+    // the issuer (it then waits for stages that have not landed: 2111).
+    // A slot's previous readers (this issuer's MMAs two own stages back) are
+    // fenced by dec_empty.
+    const int who = warp - 1;
     if (leader && lane == 0) {
       constexpr uint32_t idesc = idesc_i8(2 * V3_BM, V3_BT);
-      int s = 0, slot = 0;
-      uint32_t ph = 0, sph = 0;
-      int ab = 0;
+      int ab = 0, ti = 0;
       uint32_t aph = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
-        mbar_wait(&ss->acc_empty[ab], aph ^ 1);
+      int g = 0;  // global stage index of the tile's first stage
+      for (int t = pair; t < ntiles; t += npairs, ++ti, g += KB) {
+        mbar_wait(&ss->acc_empty[ab], aph);
+        if (who == 0) k3_stamp(tr, 4, ti);
         tc_fence_after();
         const uint32_t dcol = tmem + acc_col(ab);
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = ((g & 1) != who) ? 1 : 0; kb < KB; kb += 2) {
+          const int gs = g + kb;
+          const int s = gs % V3_PS;
+          const uint32_t ph = (uint32_t)(gs / V3_PS) & 1u;
           if (W8 && a.w8_ss) {  // W8A8, SS form: both operands from the stage
             mbar_wait(&ss->full[s], ph);
             tc_fence_after();
@@ -356,33 +380,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               tc_mma_pair_ss(dcol, sw128_desc(abase + kk * 32),
-                             sw128_desc(abase + V3_A_STAGE + kk * 32), idesc,
-                             (kb | kk) != 0 ? 1u : 0u);
+                             sw128_desc(abase + V3_A_STAGE + kk * 32), idesc, 1u);
             tc_commit_pair(&ss->empty[s]);
-            if (++s == V3_PS) {
-              s = 0;
-              ph ^= 1;
-            }
             continue;
           }
-          mbar_wait(&ss->dec_full[slot], sph);  // A expanded (implies the stage landed)
+          const int slot = gs % V3_SLOTS;
+          const uint32_t sph = (uint32_t)(gs / V3_SLOTS) & 1u;
+          k3_stamp(tr, 7, gs);
+          mbar_wait(&ss->full[s], ph);
+          mbar_wait(&ss->dec_empty[slot], sph ^ 1);
+          k3_stamp(tr, 3, gs);
           tc_fence_after();
-          const uint32_t bbase = smem_u32(stg + s * V3_STAGE) + V3_A_STAGE;
+          const uint32_t abase = smem_u32(stg + s * V3_STAGE);
+          const uint32_t bbase = abase + V3_A_STAGE;
           const uint32_t acol = tmem + a_col(slot);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_pair_ts(dcol, acol + kk * 8, sw128_desc(bbase + kk * 32), idesc,
-                           (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            if constexpr (W8) tc_cp_raw(acol + kk * 8, sw128_desc(abase + kk * 32));
+            else tc_cp_decompress(acol + kk * 8, sw128_desc(abase + kk * 32));
+          }
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tc_mma_pair_ts(dcol, acol + kk * 8, sw128_desc(bbase + kk * 32), idesc, 1u);
           tc_commit_pair(&ss->empty[s]);
           tc_commit_leader(&ss->dec_empty[slot]);
-          if (++s == V3_PS) {
-            s = 0;
-            ph ^= 1;
-          }
-          if (++slot == V3_SLOTS) {
-            slot = 0;
-            sph ^= 1;
-          }
+          k3_stamp(tr, 8, gs);
         }
         tc_commit_pair(&ss->acc_full[ab]);
         if (++ab == 2) {
@@ -391,52 +412,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
         }
       }
     }
-  } else if (warp == 3) {
-    // ===== decompress issuer (leader): padded int4 smem -> int8 TMEM ========
-    // A separate issuing thread, so the copies can run beside the MMAs.
-    if (leader && lane == 0 && !(W8 && a.w8_ss)) {
-      int s = 0, slot = 0;
-      uint32_t ph = 0, sph = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
-        for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&ss->full[s], ph);
-          mbar_wait(&ss->dec_empty[slot], sph ^ 1);
-          tc_fence_after();
-          const uint32_t abase = smem_u32(stg + s * V3_STAGE);
-          const uint32_t acol = tmem + a_col(slot);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            if constexpr (W8) tc_cp_raw(acol + kk * 8, sw128_desc(abase + kk * 32));
-            else tc_cp_decompress(acol + kk * 8, sw128_desc(abase + kk * 32));
-          }
-          tc_commit_leader(&ss->dec_full[slot]);
-          if (++s == V3_PS) {
-            s = 0;
-            ph ^= 1;
-          }
-          if (++slot == V3_SLOTS) {
-            slot = 0;
-            sph ^= 1;
-          }
-        }
-      }
-    }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> dequant -> direct stores =======================
     // Lane = output channel, so for each token the warp's 32 lanes write 32
     // consecutive channels (64 B bf16 / 128 B f32): coalesced without a
-    // transpose.  Two warps per TMEM lane quarter split the token chunks.
+    // transpose or shared-memory staging (staging boxes for TMA stores
+    // would cost the eighth operand stage).  Two warps per TMEM lane
+    // quarter split the token chunks.
     const int q = warp & 3;
     const int h = (warp - 4) >> 2;
     const int et = threadIdx.x - 128;  // 0..255
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
-    const uint32_t ybuf = smem_u32(ystg) + (uint32_t)(warp - 4) * V3_YSTG;
     // fdq: integer-to-float by the magic constant, two tokens per fp32x2
     // instruction; exact while |4*sum(w*a)| < 2^22 (4*49*K < 2^22: K <= 21384)
-    const bool fdq = !W8 && a.y_tma && a.fdq && a.K <= 21384;
-    int ab = 0;
+    const bool fdq = !W8 && a.out_kind == 0 && a.fdq && a.K <= 21384;
+    int ab = 0, ti = 0;
     uint32_t aph = 0;
-    for (int t = pair; t < ntiles; t += npairs) {
+    unsigned long long* const etr = (warp == 4 && lane == 0) ? tr : nullptr;
+    // both accumulators start at zero (the MMAs never overwrite), then
+    // release them to the issuers (phase 0 of acc_empty)
+    for (int b2 = 0; b2 < 2; ++b2)
+      for (int c = h; c < V3_BT / 32; c += 2) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(b2) + c * 32);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      arrive_cluster(empty_acc);
+      arrive_cluster(empty_acc + 8);
+    }
+    for (int t = pair; t < ntiles; t += npairs, ++ti) {
       const int tt = t % a.ttiles, ct = t / a.ttiles;
       const int64_t mb = (int64_t)tt * V3_BT;                                // tile tokens
       const int64_t nw = (int64_t)ct * 2 * V3_BM + (int64_t)rank * V3_BM + q * 32;  // warp's channels
@@ -444,69 +448,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
       const bool nok = n < a.N;
       const float sw = nok ? a.w_scales[n] : 0.f;
       const float bn = (a.bias && nok) ? a.bias[n] : 0.f;
+      named_bar_sync(2, 256);  // every epilogue warp is done with the previous tile's token data
       for (int i = et; i < V3_BT; i += 256) {
         const int64_t m = mb + i;
-        ss->sa[ab][i] = m < a.M ? a.a_scales[m] : 0.f;
+        ss->sa[i] = m < a.M ? a.a_scales[m] : 0.f;
         const int off = (W8 || m >= a.M) ? 0 : 32 * a.a_sums[m];
         // magic-number dequant (fdq): acc' + (0x4B400000 - 32 S_a) are the
         // float bits of 1.5*2^23 + 4*sum(w*a)
-        ss->sums[ab][i] = fdq ? (int)(0x4B400000u - (uint32_t)off) : off;
+        ss->sums[i] = fdq ? (int)(0x4B400000u - (uint32_t)off) : off;
       }
       named_bar_sync(1, 256);
       wait_sleep(&ss->acc_full[ab], aph);
+      k3_stamp(etr, 5, ti);
       tc_fence_after();
 #pragma unroll 1
       for (int c = h; c < V3_BT / 32; c += 2) {
         uint32_t acc[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32, acc);
+        tmem_zero32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32);
         const int64_t m0 = mb + c * 32;  // tokens m0 .. m0+31 of this chunk
-        if (a.y_tma) {
-          // bf16 box via shared memory + one TMA store; the tensor map clips
-          // tokens >= M and channels >= N (their staged values are unused)
-          if (m0 >= a.M || nw >= a.N) continue;
-          uint32_t sav[32], smv[32];
-          lds_row32(smem_u32(&ss->sa[ab][c * 32]), sav);
-          if constexpr (!W8) lds_row32(smem_u32(&ss->sums[ab][c * 32]), smv);
-          if (lane == 0) bulk_wait_read0();  // the previous box has left the buffer
-          __syncwarp();
-          if (fdq) {
-            // v = (acc' - 32 S_a) / 4 exactly: fma(1.5*2^23 + 4v, 1/4, -1.5*2^21);
-            // then the same fp32 expression as below, two tokens at a time
-            const float2 q4 = make_float2(0.25f, 0.25f), mc = make_float2(-3145728.f, -3145728.f);
-            const float2 w2 = make_float2(sw, sw), b2 = make_float2(bn, bn);
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const float2 mm = make_float2(__uint_as_float(acc[j] + smv[j]),
-                                            __uint_as_float(acc[j + 1] + smv[j + 1]));
-              const float2 v = __ffma2_rn(mm, q4, mc);
-              const float2 p =
-                  __fmul2_rn(v, make_float2(__uint_as_float(sav[j]), __uint_as_float(sav[j + 1])));
-              const __nv_bfloat162 o = __float22bfloat162_rn(__ffma2_rn(p, w2, b2));
-              st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o.x));
-              st_shared_u16(ybuf + (uint32_t)(j + 1) * 64u + (uint32_t)lane * 2u,
-                            __bfloat16_as_ushort(o.y));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
-              const __nv_bfloat16 o =
-                  __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
-              st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o));
-            }
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&map_y, ybuf, (int)nw, (int)m0);
-            bulk_commit();
-          }
-          continue;
-        }
-        if (m0 >= a.M || !nok) continue;
+        if (m0 >= a.M || !nok || a.dbg_skip_epi) continue;
         const int jn = a.M - m0 < 32 ? (int)(a.M - m0) : 32;
-        const int* sm = &ss->sums[ab][c * 32];
-        const float* sa = &ss->sa[ab][c * 32];
+        const int* sm = &ss->sums[c * 32];
+        const float* sa = &ss->sa[c * 32];
         if (a.out_kind == 0) {
           __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(a.y) + m0 * a.ldy + n;
           if (jn == 32) {
@@ -515,16 +479,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
             uint32_t sav[32], smv[32];
             lds_row32(smem_u32(sa), sav);
             if constexpr (!W8) lds_row32(smem_u32(sm), smv);
+            if (fdq) {
+              // v = (acc' - 32 S_a) / 4 exactly: fma(1.5*2^23 + 4v, 1/4, -1.5*2^21);
+              // then the same fp32 expression as below, two tokens at a time
+              const float2 q4 = make_float2(0.25f, 0.25f), mc = make_float2(-3145728.f, -3145728.f);
+              const float2 w2 = make_float2(sw, sw), b2 = make_float2(bn, bn);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
-              yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
+              for (int j = 0; j < 32; j += 2) {
+                const float2 mm = make_float2(__uint_as_float(acc[j] + smv[j]),
+                                              __uint_as_float(acc[j + 1] + smv[j + 1]));
+                const float2 v = __ffma2_rn(mm, q4, mc);
+                const float2 p =
+                    __fmul2_rn(v, make_float2(__uint_as_float(sav[j]), __uint_as_float(sav[j + 1])));
+                const __nv_bfloat162 o = __float22bfloat162_rn(__ffma2_rn(p, w2, b2));
+                yp[j * a.ldy] = o.x;
+                yp[(j + 1) * a.ldy] = o.y;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int v = W8 ? (int)acc[j] : (((int)acc[j] - (int)smv[j]) >> 2);
+                yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
+              }
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (j < jn) {
-                const int v = W8 ? (int)acc[j] : (((int)acc[j] - sm[j]) >> 2);
+                // fdq offsets hold 0x4B400000 - 32 S_a: recover 32 S_a
+                const int off = fdq ? (int)(0x4B400000u - (uint32_t)sm[j]) : sm[j];
+                const int v = W8 ? (int)acc[j] : (((int)acc[j] - off) >> 2);
                 yp[j * a.ldy] = __float2bfloat16_rn(fmaf((float)v * sa[j], sw, bn));
               }
           }
@@ -539,15 +523,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
             }
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
+      k3_stamp(etr, 6, ti);
       if (lane == 0) arrive_cluster(empty_acc + ab * 8);
       if (++ab == 2) {
         ab = 0;
         aph ^= 1;
       }
     }
-    if (a.y_tma && lane == 0) bulk_wait0();  // every box written before the CTA exits
   }
 
   tc_fence_before();
@@ -574,7 +559,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_v3() {
   return fn;
 }
 
+std::atomic<unsigned long long*> g_k3_trace{nullptr};
 }  // namespace
+
+void set_k3_trace(unsigned long long* buf) { g_k3_trace.store(buf); }
+unsigned long long* k3_trace() { return g_k3_trace.load(); }
 
 bool k3_v3_supported(const K3Args& a) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.K > 1277000) return false;
@@ -622,25 +611,7 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  // bf16 output map: N channels (inner) x M tokens, 32 x 32 boxes
-  CUtensorMap my = mx;
-  static const bool direct_stores = [] {  // A/B switch: the per-lane direct stores
-    const char* e = getenv("CRT_K3_DIRECT_STORES");
-    return e && e[0] == '1';
-  }();
-  bool y_tma = false;
-  if (a.out_kind == 0 && !direct_stores && (uintptr_t)a.y % 16 == 0 && (a.ldy * 2) % 16 == 0) {
-    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
-    cuuint64_t strides[1] = {(cuuint64_t)(a.ldy * 2)};
-    cuuint32_t box[2] = {32, 32};
-    cuuint32_t es[2] = {1, 1};
-    y_tma = fn(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.y, dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    if (!y_tma) my = mx;
-  }
   V3Args v{};
-  v.y_tma = y_tma ? 1 : 0;
   static const bool no_fdq = [] {  // A/B switch: per-token I2F dequant
     const char* e = getenv("CRT_K3_NO_FDQ");
     return e && e[0] == '1';
@@ -663,8 +634,14 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
     return e && e[0] == '1';
   }();
   v.w8_ss = w8 && !w8_ts;
+  v.trace = k3_trace();
+  static const bool skip_epi = [] {
+    const char* e = getenv("CRT_K3_DBG_SKIP_EPI");
+    return e && e[0] == '1';
+  }();
+  v.dbg_skip_epi = skip_epi ? 1 : 0;
   const size_t smem =
-      1024 + V3_PS * V3_STAGE + ((sizeof(V3Smem) + 127) & ~(size_t)127) + 8 * V3_YSTG;
+      1024 + V3_PS * V3_STAGE + ((sizeof(V3Smem) + 127) & ~(size_t)127);
   auto kern = w8 ? k3_v3_kernel<true> : k3_v3_kernel<false>;
   static SmemAttr attr[2];
   {
@@ -675,7 +652,7 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
   const cudaError_t le = launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(V3_THREADS), smem, st,
-                                    mw, mx, my, v);
+                                    mw, mx, v);
   ++*launches;
   return le;
 }

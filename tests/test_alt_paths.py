@@ -1,8 +1,8 @@
 """Opt-in kernel paths stay bit-exact: the mma.sync K1 (CRT_K1_MMA=1), the
 tcgen05 tensor-core K1 (CRT_K1_TC=1), the round-1 rolled K1 (CRT_K1_TEAM=0),
 the register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
-(CRT_K3_V1=1), the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-lane
-store epilogue (CRT_K3_DIRECT_STORES=1), each -- and the defaults -- in a fresh
+(CRT_K3_V1=1), the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-token
+I2F dequant (CRT_K3_NO_FDQ=1), each -- and the defaults -- in a fresh
 process."""
 import os
 import subprocess
@@ -16,8 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K1_TC": "1"},
                                  {"CRT_K1_TEAM": "0"}, {"CRT_K3_V1": "1"},
-                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_DIRECT_STORES": "1"},
-                                 {"CRT_K3_NO_FDQ": "1"}])
+                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_NO_FDQ": "1"}])
 def test_opt_in_paths_bit_exact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
@@ -27,11 +26,10 @@ def test_opt_in_paths_bit_exact(env):
 
 @pytest.mark.gpu
 def test_epilogue_variants_bit_identical_bf16():
-    """The TMA-store epilogue with the magic-number dequant (default), with
-    the per-token I2F dequant (CRT_K3_NO_FDQ=1) and the per-lane direct
-    stores (CRT_K3_DIRECT_STORES=1) write the same bf16 bits."""
+    """The epilogue with the magic-number dequant (default) and with the
+    per-token I2F dequant (CRT_K3_NO_FDQ=1) write the same bf16 bits."""
     digests = []
-    for env in ({}, {"CRT_K3_NO_FDQ": "1"}, {"CRT_K3_DIRECT_STORES": "1"}):
+    for env in ({}, {"CRT_K3_NO_FDQ": "1"}):
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
                            cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)

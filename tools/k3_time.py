@@ -9,7 +9,7 @@ from paper_2512_03673_b200 import RotationKind, RotationSpec  # noqa: E402
 
 spec = RotationSpec(RotationKind.regular, 16)
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
-for M, K, N in [(4608, 3072, 12288), (4608, 12288, 3072), (4608, 3072, 3072)]:
+for M, K, N in [(4608, 3072, 12288), (4608, 12288, 3072), (4608, 3072, 3072), (4096, 3072, 3072)]:
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     layer = crt.prepare_layer(torch.randn(N, K, device="cuda").to(torch.bfloat16), None, spec)
     c, sa, su = crt.rotate_quantize_i8(x, spec)
