@@ -350,12 +350,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V3_THREADS, 1)
     // the other's first MMA of a tile.  acc_full takes one commit from each.
     // Each issuer also expands the A operand of its stage (tcgen05.cp from
     // the padded smem stage into a TMEM slot) right before the stage's
-    // MMAs: cp -> mma from one thread execute in order.  Measured and
-    // rejected: one separate expansion thread (its own waits drain its
-    // copies: ~580 cycles per stage), two expansion threads (the copies queue
-    // behind the MMAs already issued, so the issuers wait ~900 cycles for
-    // them: 2757 vs 2819 TOPS at fc1), and expanding two stages ahead inside
-    // the issuer (it then waits for stages that have not landed: 2111).
+    // MMAs: cp -> mma from one thread execute in order.  The copies cost
+    // tensor-pipe time (ncu at fc1: tc pipe 85% busy, MMA 65%), but every
+    // ordering that issues them earlier measured slower (fc1 TOPS, k3_time):
+    // one separate expansion thread (its own waits drain its copies: ~580
+    // cycles per stage), two expansion threads (copies queue behind issued
+    // MMAs; issuers wait ~900 cycles: 2757 vs 2819), an issuer expanding its
+    // own next stage (2111), expanding the other issuer's next stage (2248),
+    // and issuing each stage's MMAs one own step after its copies (~1650 at
+    // 3072^2 vs 2110).
     // A slot's previous readers (this issuer's MMAs two own stages back) are
     // fenced by dec_empty.
     const int who = warp - 1;

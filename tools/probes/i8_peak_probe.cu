@@ -917,6 +917,106 @@ void run_same_d(int sms) {
   }
 }
 
+
+// K3's inline pattern with 1..4 issuing threads (warps 0..3 of the leader),
+// all into ONE accumulator (as K3): per 4-MMA stage each issuer waits,
+// expands its stage's A (4 decompress copies into its own 32-column slot),
+// issues the 4 dependent MMAs and 2 commits.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_n_issuers(int iters, int nissuers, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[4], done_bar, cbar[8];
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = t; i < (128 + 96) * 128 / 4; i += 128) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int k = 0; k < 4; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[k])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done_bar)));
+    for (int k = 0; k < 8; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(smem_u32(&cbar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&done_bar)) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint64_t b = sw128_desc(smem_u32(sm + 128 * 128));
+  const uint64_t adesc = sw128_desc(smem_u32(sm));
+  const int who = warp;
+  if (rank == 0 && lane == 0 && who < nissuers) {
+    const uint32_t id = idesc(true, 256, 192);
+    const uint32_t d = tmem_base;
+    const uint32_t aslot = tmem_base + 192 + (uint32_t)who * 32;
+    const unsigned long long c0 = clock64();
+    for (int st = who; st < iters / 4; st += nissuers) {
+      asm volatile(
+          "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+          "@!P1 bra W_%=;\n}\n" ::"r"(smem_u32(&done_bar))
+          : "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int k = 0; k < 4; ++k)
+        asm volatile("tcgen05.cp.cta_group::2.128x256b.b8x16.b4x16_p64 [%0], %1;" ::"r"(aslot + k * 8),
+                     "l"(adesc + (uint64_t)(k * 2))
+                     : "memory");
+      for (int k = 0; k < 4; ++k)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+            "r"(aslot + (uint32_t)k * 8), "l"(b + (uint64_t)(k * 2)), "r"(id), "r"(1));
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&cbar[2 * who])), "h"((uint16_t)3)
+          : "memory");
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&cbar[2 * who + 1])), "h"((uint16_t)1)
+          : "memory");
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&bar[who])), "h"((uint16_t)1)
+        : "memory");
+    asm volatile(
+        "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra W_%=;\n}\n" ::"r"(smem_u32(&bar[who]))
+        : "memory");
+    cycles[4 * blockIdx.x + who] = clock64() - c0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+void run_n(int sms, int n) {
+  const int iters = 20000;
+  const size_t smem = (size_t)(128 + 96) * 128;
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sms * 32);
+  cudaMemset(cyc, 0, sms * 32);
+  cudaFuncSetAttribute(mma_n_issuers, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_n_issuers<<<sms, 128, smem>>>(100, n, cyc);
+  cudaDeviceSynchronize();
+  mma_n_issuers<<<sms, 128, smem>>>(iters, n, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long c[4];
+  cudaMemcpy(c, cyc, 32, cudaMemcpyDeviceToHost);
+  unsigned long long cm = 0;
+  for (int k = 0; k < n; ++k) cm = c[k] > cm ? c[k] : cm;
+  printf("%d issuers, K3 inline stage (wait, 4 cps, 4 dependent MMAs, 2 commits), one accumulator: %.1f cycles per MMA (ideal 96) err=%s\n",
+         n, (double)cm / iters, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(cyc);
+}
+
 template <bool I8, int N>
 void run(int sms) {
   const int iters = 20000;
@@ -967,6 +1067,7 @@ int main() {
   run_gap<11>(sms, 0);
   run_gap<12>(sms, 0);
   run_gap<13>(sms, 0);
+  for (int n = 1; n <= 4; ++n) run_n(sms, n);
   run_same_d(sms);
   run_two(sms, 1);
   run_two(sms, 2);
