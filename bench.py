@@ -652,7 +652,16 @@ def run_ours(args):
         pass
     bf16_burst = float(peaks.get("bf16_tflops", 1590.0))
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    int8_peak = 2.0 * bf16_burst  # tcgen05 kind::i8 runs at 2x the kind::f16 rate
+    # the dense INT8 tensor ceiling measured directly (tools/probes/i8_peak_probe.cu,
+    # profiles/int8_ceiling.json); 2 x the cuBLAS bf16 burst only if that file is absent
+    int8_peak, int8_src = 2.0 * bf16_burst, "2 x measured bf16 burst (MEASURED_PEAKS.json)"
+    try:
+        int8_peak = float(json.load(open(os.path.join(ROOT, "profiles", "int8_ceiling.json")))[
+            "kind_i8_tops"])
+        int8_src = ("tcgen05 kind::i8 back-to-back MMA ceiling measured on this part "
+                    "(tools/probes/i8_peak_probe.cu, profiles/int8_ceiling.json)")
+    except Exception:
+        pass
     # bf16 in + codes out + fp32 scale (+ int32 code sum for v3) per row
     k1_bytes = {k: M_TOK * kk * (2 + cpb) + (8 if v3 else 4) * M_TOK
                 for k, kk in (("fc1", D_MODEL), ("fc2", D_FF))}
@@ -785,7 +794,7 @@ def run_ours(args):
                          "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per fc1 "
                                             "launch from an ncu --set full capture "
                                             "(profiles/k3_traffic.json); not measured in this run"),
-                         "peak_note": "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json); "
+                         "peak_note": f"int8 dense = {int8_src}; "
                                       f"vs nominal 4500: {k3_tops / 4500:.3f}",
                          "ops_per_launch": k3_ops_per_launch, "avg_launch_us": k3_us},
             "k1_roofline": k1_roof,
