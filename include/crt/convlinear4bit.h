@@ -323,7 +323,7 @@ int64_t crt_launch_count(void);
  * barrier passed, row done, for the first 8 rows).  NULL turns it off. */
 void crt_debug_k1_trace(void* buf);
 /* Dev aid: K3 (v3) clock64 stamps of the first CTA pair's leader CTA into
- * buf (9 x 4096 uint64: per stage and per tile, see k3_gemm_v3.cu).  NULL
+ * buf (11 x 4096 uint64: per stage and per tile, see k3_gemm_v3.cu).  NULL
  * turns it off. */
 void crt_debug_k3_trace(void* buf);
 int32_t crt_abi_version(void);

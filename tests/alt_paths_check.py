@@ -1,6 +1,6 @@
 """Parity of the opt-in kernel paths, run in a subprocess by
 tests/test_alt_paths.py with CRT_K1_MMA=1 / CRT_K1_FAST=1 / CRT_K3_V1=1 /
-CRT_K3_W8_TS=1 / CRT_K3_NO_FDQ=1 (or nothing: the default paths) set before the library loads (the switches are read once per
+CRT_K3_V3=1 / CRT_K3_W8_TS=1 / CRT_K3_NO_FDQ=1 (or nothing: the default paths) set before the library loads (the switches are read once per
 process).  W4A4 against the oracle; W8A8 accumulators against the exact
 integer GEMM of the exported codes."""
 import hashlib

@@ -1,9 +1,9 @@
 """Opt-in kernel paths stay bit-exact: the mma.sync K1 (CRT_K1_MMA=1), the
 tcgen05 tensor-core K1 (CRT_K1_TC=1), the round-1 rolled K1 (CRT_K1_TEAM=0),
 the register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
-(CRT_K3_V1=1), the TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-token
-I2F dequant (CRT_K3_NO_FDQ=1), each -- and the defaults -- in a fresh
-process."""
+(CRT_K3_V1=1), the round-2 hardware-expansion W4A4 K3 (CRT_K3_V3=1), the
+TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-token I2F dequant
+(CRT_K3_NO_FDQ=1), each -- and the defaults -- in a fresh process."""
 import os
 import subprocess
 import sys
@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K1_TC": "1"},
                                  {"CRT_K1_TEAM": "0"}, {"CRT_K3_V1": "1"},
-                                 {"CRT_K3_W8_TS": "1"}, {"CRT_K3_NO_FDQ": "1"}])
+                                 {"CRT_K3_V3": "1"}, {"CRT_K3_W8_TS": "1"},
+                                 {"CRT_K3_NO_FDQ": "1"}])
 def test_opt_in_paths_bit_exact(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
@@ -26,10 +27,11 @@ def test_opt_in_paths_bit_exact(env):
 
 @pytest.mark.gpu
 def test_epilogue_variants_bit_identical_bf16():
-    """The epilogue with the magic-number dequant (default) and with the
-    per-token I2F dequant (CRT_K3_NO_FDQ=1) write the same bf16 bits."""
+    """The v4 epilogue with the magic-number dequant (default), with the
+    per-token I2F dequant (CRT_K3_NO_FDQ=1), and the v3 kernel
+    (CRT_K3_V3=1) write the same bf16 bits."""
     digests = []
-    for env in ({}, {"CRT_K3_NO_FDQ": "1"}):
+    for env in ({}, {"CRT_K3_NO_FDQ": "1"}, {"CRT_K3_V3": "1"}):
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "alt_paths_check.py")],
                            cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)

@@ -25,14 +25,14 @@ y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 for _ in range(3):
     crt.quant_gemm_i8(c, sa, su, layer, y=y)
 lib = _abi.load()
-tr = torch.zeros(9 * T, dtype=torch.int64, device="cuda")
+tr = torch.zeros(11 * T, dtype=torch.int64, device="cuda")
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
 flush.zero_()
 lib.crt_debug_k3_trace(ctypes.c_void_p(tr.data_ptr()))
 crt.quant_gemm_i8(c, sa, su, layer, y=y)
 torch.cuda.synchronize()
 lib.crt_debug_k3_trace(None)
-t = tr.view(9, T).cpu().numpy().astype(np.float64)
+t = tr.view(11, T).cpu().numpy().astype(np.float64)
 KB = (K + 127) // 128
 ns = int((t[3] > 0).sum())
 nt = int((t[4] > 0).sum())
@@ -43,9 +43,23 @@ print(f"M={M} K={K} N={N}: {ns} stages, {nt} tiles on pair 0, KB={KB}; "
 print(f"  first MMA issue at {MI[0]:.0f} cycles after the first producer issue; "
       f"last MMA issue at {MI[-1]:.0f}")
 lo, hi = KB, ns  # steady state: skip the first tile
-for name, v in (("producer issue", P), ("MMA issue", MI)):
+rows = [("producer issue", P), ("MMA issue", MI)]
+v4 = (t[9, :ns] > 0).all()
+if (t[1, :ns] > 0).all() and not v4:
+    rows[1:1] = [("expander sees full", DF), ("expander done", DI)]
+for name, v in rows:
     d = np.diff(v[lo:hi])
     print(f"  {name:17s}: median {np.median(d):6.0f}  mean {d.mean():6.0f}  p90 {np.percentile(d, 90):6.0f} cycles/stage")
+if (t[1, :ns] > 0).all() and not v4:
+    print(f"  producer issue -> expander sees stage: median {np.median((DF - P)[lo:hi]):.0f}; "
+          f"expansion time median {np.median((DI - DF)[lo:hi]):.0f}; expander done -> MMA issue "
+          f"median {np.median((MI - DI)[lo:hi]):.0f}")
+if v4:  # globaltimer ns, both CTAs of pair 0
+    LF, LD, PF, PD = t[1, :ns], t[2, :ns], t[9, :ns], t[10, :ns]
+    print(f"  v4 expanders (ns): leader stage period {np.median(np.diff(LF[lo:hi])):.0f}, expansion "
+          f"{np.median((LD - LF)[lo:hi]):.0f}; peer sees each stage {np.median((PF - LF)[lo:hi]):.0f} "
+          f"after the leader, finishes {np.median((PD - LD)[lo:hi]):.0f} after, expansion "
+          f"{np.median((PD - PF)[lo:hi]):.0f}")
 ring = MI[lo:hi] - P[lo:hi]
 print(f"  producer issue -> MMA issue (stage age at use): median {np.median(ring):.0f}")
 W0, W1 = t[7, :ns] - t0, t[8, :ns] - t0
