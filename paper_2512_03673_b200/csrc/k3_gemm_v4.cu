@@ -42,7 +42,11 @@ namespace crt {
 namespace {
 
 constexpr int V4_BM = 128;         // channels per CTA (pair: 256)
-constexpr int V4_BT = 192;         // tokens per pair tile
+#ifndef CRT_K3_V4_BT
+#define CRT_K3_V4_BT 192
+#endif
+constexpr int V4_BT = CRT_K3_V4_BT;  // tokens per pair tile (224, one slot per expander
+                                     // group: 2108 vs 3032 TOPS at fc1)
 constexpr int V4_BTH = V4_BT / 2;  // token rows of B per CTA
 constexpr int V4_PS = 10;          // stages
 constexpr int V4_EPI_WARPS = 4;    // epilogue warps 4..7 (one per TMEM lane quarter)
@@ -56,7 +60,7 @@ static_assert(V4_STAGE % 1024 == 0 && V4_AP % 1024 == 0, "swizzled tiles need 10
 // TMEM (512 columns): accumulators at 0 and 256 (V4_BT columns each), the
 // rest of each half holds 32-column A slots (one 128-code K block each)
 constexpr int V4_SLOTS = (256 - V4_BT) / 32 * 2;
-static_assert(V4_SLOTS == 4, "two A slots per accumulator half");
+static_assert(V4_SLOTS == 2 || V4_SLOTS == 4, "one or two A slots per accumulator half");
 
 struct V4Smem {
   uint64_t full[V4_PS];      // each CTA: its own TMA bytes (A packed + B)
@@ -72,7 +76,8 @@ struct V4Smem {
 
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
 __device__ __forceinline__ uint32_t a_col(int s) {
-  return (s < 2 ? (uint32_t)V4_BT : 256u + (uint32_t)V4_BT) + (uint32_t)(s & 1) * 32u;
+  constexpr int H = V4_SLOTS / 2;
+  return (s < H ? (uint32_t)V4_BT : 256u + (uint32_t)V4_BT) + (uint32_t)(s % H) * 32u;
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
