@@ -42,42 +42,65 @@ namespace crt {
 namespace {
 
 constexpr int V4_BM = 128;         // channels per CTA (pair: 256)
-#ifndef CRT_K3_V4_BT
-#define CRT_K3_V4_BT 192
-#endif
-constexpr int V4_BT = CRT_K3_V4_BT;  // tokens per pair tile (224, one slot per expander
-                                     // group: 2108 vs 3032 TOPS at fc1)
-constexpr int V4_BTH = V4_BT / 2;  // token rows of B per CTA
 constexpr int V4_PS = 10;          // stages
 constexpr int V4_EPI_WARPS = 4;    // epilogue warps 4..7 (one per TMEM lane quarter)
 constexpr int V4_EXP_WARPS = 8;    // expander warps per CTA: 3 and 8..14, two groups of 4
 constexpr int V4_THREADS = 32 * (4 + V4_EPI_WARPS + V4_EXP_WARPS - 1);
 constexpr int V4_EPI_THREADS = 32 * V4_EPI_WARPS;
 constexpr int V4_AP = V4_BM * 64;        // 8 KB: packed A, 128 rows x 64 B (128 codes), 64B swizzle
-constexpr int V4_B = V4_BTH * 128;       // 12 KB: int8 activation codes, 128B swizzle
-constexpr int V4_STAGE = V4_AP + V4_B;   // 20 KB (1024-aligned)
-static_assert(V4_STAGE % 1024 == 0 && V4_AP % 1024 == 0, "swizzled tiles need 1024-B alignment");
-// TMEM (512 columns): accumulators at 0 and 256 (V4_BT columns each), the
-// rest of each half holds 32-column A slots (one 128-code K block each)
-constexpr int V4_SLOTS = (256 - V4_BT) / 32 * 2;
-static_assert(V4_SLOTS == 2 || V4_SLOTS == 4, "one or two A slots per accumulator half");
+// Token-tile width BT (tokens per pair tile) is a template parameter: 192
+// by default, 176 where it saves a wave (k3_v4_pick_bt).  224 measured
+// slower (one A slot per expander group: 2108 vs 3032 TOPS at fc1).
+template <int BT>
+struct V4Cfg {
+  static constexpr int BTH = BT / 2;                            // token rows of B per CTA
+  static constexpr int B = BTH * 128;                           // int8 activation codes, 128B swizzle
+  static constexpr int STAGE = (V4_AP + B + 1023) / 1024 * 1024;  // packed A | B, 1024-aligned
+  // TMEM (512 columns): accumulators at 0 and 256 (BT columns each), the
+  // rest of each half holds 32-column A slots (one 128-code K block each)
+  static constexpr int SLOTS = (256 - BT) / 32 * 2;
+  static constexpr int NCH = (BT + 31) / 32;                    // epilogue token chunks
+  static constexpr int LASTW = BT - 32 * (NCH - 1);             // width of the last one
+  static_assert(SLOTS == 4, "two A slots per accumulator half");
+  static_assert(LASTW == 32 || LASTW == 16, "chunks of 32 (+ one of 16)");
+  static_assert(BT % 16 == 0 && BT <= 192, "UMMA N");
+};
 
+template <int BT>
 struct V4Smem {
   uint64_t full[V4_PS];      // each CTA: its own TMA bytes (A packed + B)
   uint64_t empty[V4_PS];     // both: MMA commit multicast
-  uint64_t slot_full[V4_SLOTS];   // leader: A slot written (4 expander warps x 2 CTAs)
-  uint64_t slot_empty[V4_SLOTS];  // both: MMA commit multicast
+  uint64_t slot_full[4];     // leader: A slot written (4 expander warps x 2 CTAs)
+  uint64_t slot_empty[4];    // both: MMA commit multicast
   uint64_t acc_full[2];      // both: one commit per MMA issuer
   uint64_t acc_empty[2];     // leader: 8 epilogue warps x 2 CTAs
   uint32_t tmem_base;
-  alignas(16) float sa[V4_BT];
-  alignas(16) int sums[V4_BT];
+  alignas(16) float sa[BT];
+  alignas(16) int sums[BT];
 };
 
 __device__ __forceinline__ uint32_t acc_col(int b) { return (uint32_t)b * 256u; }
+template <int BT>
 __device__ __forceinline__ uint32_t a_col(int s) {
-  constexpr int H = V4_SLOTS / 2;
-  return (s < H ? (uint32_t)V4_BT : 256u + (uint32_t)V4_BT) + (uint32_t)(s % H) * 32u;
+  return (s < 2 ? (uint32_t)BT : 256u + (uint32_t)BT) + (uint32_t)(s & 1) * 32u;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -129,9 +152,13 @@ struct V4Args {
   unsigned long long* trace;  // dev aid (crt_debug_k3_trace), as v3's layout
 };
 
+template <int BT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     k3_v4_kernel(const __grid_constant__ CUtensorMap map_w,
                  const __grid_constant__ CUtensorMap map_x, V4Args a) {
+  using C = V4Cfg<BT>;
+  constexpr int V4_BT = BT, V4_BTH = C::BTH, V4_B = C::B, V4_STAGE = C::STAGE, V4_SLOTS = C::SLOTS;
+  using V4Smem = crt::V4Smem<BT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = smem;                          // V4_PS x (packed A 8 KB | B 12 KB)
@@ -227,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
           k3_stamp(tr, 3, gs);
           tc_fence_after();
           const uint32_t bbase = smem_u32(stg + s * V4_STAGE + V4_AP);
-          const uint32_t acol = tmem + a_col(slot);
+          const uint32_t acol = tmem + a_col<BT>(slot);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             tc_mma_pair_ts(dcol, acol + kk * 8, sw128_desc(bbase + kk * 32), idesc, 1u);
@@ -277,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
       }
       mbar_wait(&ss->slot_empty[slot], ((uint32_t)(gs / V4_SLOTS) & 1u) ^ 1u);
       tc_fence_after();
-      tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col(slot), o);
+      tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col<BT>(slot), o);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -298,7 +325,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     uint32_t aph = 0;
     unsigned long long* const etr = (warp == 4 && lane == 0) ? tr : nullptr;
     for (int b2 = 0; b2 < 2; ++b2)
-      for (int c = 0; c < V4_BT / 32; ++c) tmem_zero32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(b2) + c * 32);
+      for (int c = 0; c < C::NCH; ++c) {
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc_col(b2) + c * 32;
+        if (C::LASTW == 32 || c < C::NCH - 1) tmem_zero32(ta);
+        else tmem_zero16(ta);
+      }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc_fence_before();
     __syncwarp();
@@ -326,13 +357,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
       k3_stamp(etr, 5, ti);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < V4_BT / 32; ++c) {
+      for (int c = 0; c < C::NCH; ++c) {
         uint32_t acc[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32, acc);
-        tmem_zero32(tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32);
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32;
+        const int cw = (C::LASTW == 32 || c < C::NCH - 1) ? 32 : 16;  // chunk width
+        if (cw == 32) {
+          tmem_ld32(ta, acc);
+          tmem_zero32(ta);
+        } else {
+          tmem_ld16(ta, acc);
+          tmem_zero16(ta);
+        }
         const int64_t m0 = mb + c * 32;
         if (m0 >= a.M || !nok) continue;
-        const int jn = a.M - m0 < 32 ? (int)(a.M - m0) : 32;
+        const int jn = a.M - m0 < cw ? (int)(a.M - m0) : cw;
         const int* sm = &ss->sums[c * 32];
         const float* sa = &ss->sa[c * 32];
         if (a.out_kind == 0) {
@@ -425,8 +463,10 @@ bool k3_v4_supported(const K3Args& a) {
   return encode_fn_v4() != nullptr;
 }
 
-cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
-  const int num_sms = device_sm_count();
+namespace {
+template <int BT>
+cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int num_sms) {
+  using C = V4Cfg<BT>;
   auto fn = encode_fn_v4();
   CUtensorMap mw, mx;
   {  // weights: N rows x ld_ob bytes of packed offset-binary codes, 64 B x 128 row boxes
@@ -442,7 +482,7 @@ cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   {  // activations: M rows x K int8 codes
     cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.M};
     cuuint64_t strides[1] = {(cuuint64_t)a.lda};
-    cuuint32_t box[2] = {128, (cuuint32_t)V4_BTH};
+    cuuint32_t box[2] = {128, (cuuint32_t)C::BTH};
     cuuint32_t es[2] = {1, 1};
     if (fn(&mx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.a_codes), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -458,7 +498,7 @@ cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.M = a.M;
   v.N = a.N;
   v.K = a.K;
-  v.ttiles = (int32_t)((a.M + V4_BT - 1) / V4_BT);
+  v.ttiles = (int32_t)((a.M + BT - 1) / BT);
   v.ctiles = (int32_t)((a.N + 2 * V4_BM - 1) / (2 * V4_BM));
   v.a_scales = a.a_scales;
   v.a_sums = a.a_sums;
@@ -468,20 +508,47 @@ cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
   v.y = a.y;
   v.ldy = a.ldy;
   v.trace = k3_trace();
-  const size_t smem =
-      1024 + V4_PS * V4_STAGE + ((sizeof(V4Smem) + 127) & ~(size_t)127);
+  const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127);
   static SmemAttr attr;
   {
-    const cudaError_t e = ensure_dyn_smem(k3_v4_kernel, smem, attr, false);
+    const cudaError_t e = ensure_dyn_smem(k3_v4_kernel<BT>, smem, attr, false);
     if (e != cudaSuccess) return e;
   }
   const int tiles = v.ttiles * v.ctiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  const cudaError_t le = launch_pdl(k3_v4_kernel, dim3((unsigned)(2 * pairs)), dim3(V4_THREADS),
-                                    smem, st, mw, mx, v);
+  const cudaError_t le = launch_pdl(k3_v4_kernel<BT>, dim3((unsigned)(2 * pairs)),
+                                    dim3(V4_THREADS), smem, st, mw, mx, v);
   ++*launches;
   return le;
+}
+}  // namespace
+
+// Token-tile width: the persistent grid runs ceil(tiles / pairs) waves of
+// tiles, so the time goes as waves x BT -- but a 176-token tile does ~9%
+// less work per stage for the same fixed per-stage costs, so 176 is picked
+// only when it saves more than 10% of waves x BT.  At cfg1 (M = 4096,
+// N = 3072: 4 waves of 192 vs 4 waves of 176) the two measured equal (39.5
+// vs 38.8 us), so no FLUX shape picks it today.  CRT_K3_V4_BT=192|176 forces.
+int k3_v4_pick_bt(int64_t M, int64_t N, int num_sms) {
+  static const int forced = [] {
+    const char* e = getenv("CRT_K3_V4_BT");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 192 || forced == 176) return forced;
+  const int64_t pairs = num_sms / 2, ct = (N + 255) / 256;
+  auto cost = [&](int64_t bt) {
+    const int64_t tiles = (M + bt - 1) / bt * ct;
+    const int64_t p = tiles < pairs ? tiles : pairs;
+    return (tiles + p - 1) / p * bt;
+  };
+  return cost(176) * 11 < cost(192) * 10 ? 176 : 192;
+}
+
+cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
+  const int num_sms = device_sm_count();
+  if (k3_v4_pick_bt(a.M, a.N, num_sms) == 176) return launch_bt<176>(a, st, launches, num_sms);
+  return launch_bt<192>(a, st, launches, num_sms);
 }
 
 }  // namespace crt
