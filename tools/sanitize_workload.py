@@ -1,6 +1,6 @@
 """Small workload touching every kernel family once, for compute-sanitizer
 (memcheck / racecheck / synccheck): K1 team (bits 4 / int8-codes / 8, N0 16
-and 256, ragged K), the rolled and exact K1 paths, K3 v3 (W4A4 and W8A8), v2
+and 256, ragged K), the rolled and exact K1 paths, K3 v4 (W4A4; v3 with CRT_K3_V3=1) and v3 W8A8, v2
 and v1, the dequant / interleave kernels of the 1-rank tensor-parallel path.
 Checks the results against the plain forward as it goes."""
 import os
