@@ -51,8 +51,25 @@ def _newest(paths):
     return max((os.path.getmtime(p) for p in paths), default=0.0)
 
 
+FLAGS_STAMP = os.path.join(BUILD, "flags.txt")
+
+
+def _flags() -> str:
+    """The compile command line objects are built with; a change (e.g. a
+    CRT_NVCC_EXTRA A/B build) invalidates every object."""
+    return " ".join(NVCC_FLAGS + os.environ.get("CRT_NVCC_EXTRA", "").split())
+
+
+def _flags_changed() -> bool:
+    try:
+        with open(FLAGS_STAMP) as f:
+            return f.read() != _flags()
+    except OSError:
+        return True
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or _flags_changed():
         return True
     return _newest(_sources() + _headers() + [__file__]) > os.path.getmtime(LIB)
 
@@ -75,6 +92,8 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = True) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
+    if _flags_changed():
+        force = True
     srcs = _sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     if verbose:
@@ -87,6 +106,8 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = True) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(FLAGS_STAMP, "w") as f:
+        f.write(_flags())
     if verbose:
         print(f"[build] wrote {LIB}", file=sys.stderr)
     return LIB
