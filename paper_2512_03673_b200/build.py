@@ -51,7 +51,8 @@ def _newest(paths):
     return max((os.path.getmtime(p) for p in paths), default=0.0)
 
 
-FLAGS_STAMP = os.path.join(BUILD, "flags.txt")
+# next to the library (it travels with it; _build/ does not)
+FLAGS_STAMP = LIB[:-3] + ".flags"
 
 
 def _flags() -> str:
