@@ -150,7 +150,6 @@ struct V4Args {
   int64_t ldy;
   int32_t fdq;       // magic-number fp32x2 dequant (bf16 output)
   unsigned long long* trace;  // dev aid (crt_debug_k3_trace), as v3's layout
-  int32_t dbg_nozero;         // dev aid (CRT_K3_V4_NOZERO=1): skip the per-tile zeroing (wrong output)
 };
 
 template <int BT>
@@ -364,10 +363,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
         const int cw = (C::LASTW == 32 || c < C::NCH - 1) ? 32 : 16;  // chunk width
         if (cw == 32) {
           tmem_ld32(ta, acc);
-          if (!a.dbg_nozero) tmem_zero32(ta);
+          tmem_zero32(ta);
         } else {
           tmem_ld16(ta, acc);
-          if (!a.dbg_nozero) tmem_zero16(ta);
+          tmem_zero16(ta);
         }
         const int64_t m0 = mb + c * 32;
         if (m0 >= a.M || !nok) continue;
@@ -509,11 +508,6 @@ cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int n
   v.y = a.y;
   v.ldy = a.ldy;
   v.trace = k3_trace();
-  static const bool nozero = [] {
-    const char* e = getenv("CRT_K3_V4_NOZERO");
-    return e && e[0] == '1';
-  }();
-  v.dbg_nozero = nozero ? 1 : 0;
   const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127);
   static SmemAttr attr;
   {
