@@ -56,9 +56,11 @@ FLAGS_STAMP = LIB[:-3] + ".flags"
 
 
 def _flags() -> str:
-    """The compile command line objects are built with; a change (e.g. a
-    CRT_NVCC_EXTRA A/B build) invalidates every object."""
-    return " ".join(NVCC_FLAGS + os.environ.get("CRT_NVCC_EXTRA", "").split())
+    """The compile flags objects are built with, without the (checkout-
+    dependent) include paths; a change (e.g. a CRT_NVCC_EXTRA A/B build)
+    invalidates every object."""
+    return " ".join(f for f in NVCC_FLAGS + os.environ.get("CRT_NVCC_EXTRA", "").split()
+                    if not f.startswith("-I"))
 
 
 def _flags_changed() -> bool:

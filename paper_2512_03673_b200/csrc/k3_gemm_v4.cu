@@ -150,6 +150,8 @@ struct V4Args {
   int64_t ldy;
   int32_t fdq;       // magic-number fp32x2 dequant (bf16 output)
   unsigned long long* trace;  // dev aid (crt_debug_k3_trace), as v3's layout
+  int32_t dbg;                // dev aid (CRT_K3_V4_DBG bitmask, timing only, wrong output):
+                              // 1 no A-slot stores, 2 no dequant/stores, 4 no TMEM loads/zeroing
 };
 
 template <int BT>
@@ -304,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
       }
       mbar_wait(&ss->slot_empty[slot], ((uint32_t)(gs / V4_SLOTS) & 1u) ^ 1u);
       tc_fence_after();
-      tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col<BT>(slot), o);
+      if (!(a.dbg & 1)) tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col<BT>(slot), o);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -361,7 +363,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
         uint32_t acc[32];
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32;
         const int cw = (C::LASTW == 32 || c < C::NCH - 1) ? 32 : 16;  // chunk width
-        if (cw == 32) {
+        if (a.dbg & 4) {
+          continue;
+        } else if (cw == 32) {
           tmem_ld32(ta, acc);
           tmem_zero32(ta);
         } else {
@@ -369,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
           tmem_zero16(ta);
         }
         const int64_t m0 = mb + c * 32;
-        if (m0 >= a.M || !nok) continue;
+        if (m0 >= a.M || !nok || (a.dbg & 2)) continue;
         const int jn = a.M - m0 < cw ? (int)(a.M - m0) : cw;
         const int* sm = &ss->sums[c * 32];
         const float* sa = &ss->sa[c * 32];
@@ -508,6 +512,11 @@ cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int n
   v.y = a.y;
   v.ldy = a.ldy;
   v.trace = k3_trace();
+  static const int dbg = [] {
+    const char* e = getenv("CRT_K3_V4_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  v.dbg = dbg;
   const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127);
   static SmemAttr attr;
   {
