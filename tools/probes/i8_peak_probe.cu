@@ -1017,6 +1017,113 @@ void run_n(int sms, int n) {
   cudaFree(cyc);
 }
 
+
+// Pair ts MMAs (K3's shape) from one thread while warps 1..4 store into TMEM
+// A-slot columns with tcgen05.st at K3 v4's rate (4 KB per warp per 4 MMAs),
+// in shape SHAPE: 0 = 32x32b.x32, 1 = 32x32b.x8 (four per 4 KB), 2 =
+// 16x256b.x8 (16 lanes x 8 cols x 8 reps... = 4 KB per instruction pair).
+template <int SHAPE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(160, 1)
+    mma_tmem_st_loop(int iters, int store, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, warp = t >> 5;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = t; i < (128 + 96) * 128 / 4; i += 160) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint64_t b = sw128_desc(smem_u32(sm + 128 * 128));
+  const uint32_t d = tmem_base, aslot = tmem_base + 192;
+  if (rank == 0 && t == 0) {
+    const uint32_t id = idesc(true, 256, 192);
+    const unsigned long long c0 = clock64();
+    for (int i = 0; i < iters; ++i)
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+          "r"(aslot + (uint32_t)(i & 3) * 8), "l"(b + (uint64_t)((i & 3) * 2)), "r"(id), "r"(i));
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&bar)), "h"((uint16_t)1)
+        : "memory");
+    asm volatile(
+        "{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra W_%=;\n}\n" ::"r"(smem_u32(&bar))
+        : "memory");
+    cycles[blockIdx.x] = clock64() - c0;
+  }
+  if (store && warp >= 1) {  // warps 1..4: lane quarter (warp % 4); store into columns 448.. (unused)
+    const uint32_t q = (uint32_t)(warp & 3);
+    const uint32_t ta = tmem_base + 448 + (q * 32 << 16);
+    uint32_t r[32];
+    for (int k = 0; k < 32; ++k) r[k] = (uint32_t)(k * 0x01010101);
+    // K3 v4: 4 KB per warp per stage of 4 MMAs (~384 cycles); pace with the clock
+    const unsigned long long c0 = clock64();
+    for (int j = 0; j < iters / 4; ++j) {
+      while (clock64() - c0 < (unsigned long long)j * 384) {
+      }
+      if (SHAPE == 0) {
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+            "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+            "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+            "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+            "r"(r[29]), "r"(r[30]), "r"(r[31])
+            : "memory");
+      } else {
+        for (int h = 0; h < 4; ++h)
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + h * 8),
+              "r"(r[8 * h]), "r"(r[8 * h + 1]), "r"(r[8 * h + 2]), "r"(r[8 * h + 3]), "r"(r[8 * h + 4]),
+              "r"(r[8 * h + 5]), "r"(r[8 * h + 6]), "r"(r[8 * h + 7])
+              : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+template <int SHAPE>
+void run_st(int sms, int store) {
+  const int iters = 20000;
+  const size_t smem = (size_t)(128 + 96) * 128;
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sms * 8);
+  cudaFuncSetAttribute(mma_tmem_st_loop<SHAPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_tmem_st_loop<SHAPE><<<sms, 160, smem>>>(100, store, cyc);
+  cudaDeviceSynchronize();
+  mma_tmem_st_loop<SHAPE><<<sms, 160, smem>>>(iters, store, cyc);
+  cudaDeviceSynchronize();
+  unsigned long long c = 0;
+  cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("pair ts MMA + TMEM stores (%s, %s): %.1f cycles per MMA (ideal 96) err=%s\n",
+         store ? "on" : "off", SHAPE == 0 ? "32x32b.x32" : "4 x 32x32b.x8", (double)c / iters,
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(cyc);
+}
+
 template <bool I8, int N>
 void run(int sms) {
   const int iters = 20000;
@@ -1067,6 +1174,9 @@ int main() {
   run_gap<11>(sms, 0);
   run_gap<12>(sms, 0);
   run_gap<13>(sms, 0);
+  run_st<0>(sms, 0);
+  run_st<0>(sms, 1);
+  run_st<1>(sms, 1);
   for (int n = 1; n <= 4; ++n) run_n(sms, n);
   run_same_d(sms);
   run_two(sms, 1);
