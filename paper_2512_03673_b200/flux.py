@@ -150,6 +150,21 @@ class FluxStack:
                             workspace=self.ws_side if txt else self.ws, check_finite=False)
         main.wait_stream(self.side)
 
+    def capture(self) -> "torch.cuda.CUDAGraph":
+        """One CUDA graph of step() (both streams): every forward's K1 / K3
+        launches replayed without the per-call host work (the stack's 304
+        Python calls otherwise leave the GPU waiting on small units)."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.step()  # warm (tensor maps, smem attributes) outside the capture
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.step()
+        return g
+
     def output_of(self, name: str) -> Optional[torch.Tensor]:
         """The output columns of linear `name` (a view into its unit's output)."""
         for u in self.units:
