@@ -52,7 +52,9 @@ __device__ __forceinline__ uint32_t near_tie_mask_v(const float2 (&v)[16], float
   return fm;
 }
 
-template <int N0, bool F32, int BITS, bool FULL>
+// WC > 0: the team width as a compile-time constant (the FLUX widths of the
+// production instantiation), so the per-row team loops and index math fold.
+template <int N0, bool F32, int BITS, bool FULL, int WC = 0>
 __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
@@ -63,7 +65,7 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
   __shared__ int s_sum[2][kK1TMaxWarps];        // per-warp int8 code sums, by row parity
   extern __shared__ __align__(128) uint8_t k1_ring[];
 
-  const int W = blockDim.x >> 5;
+  const int W = WC > 0 ? WC : (int)(blockDim.x >> 5);
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.K / 16;
@@ -389,6 +391,20 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   const size_t rb = (size_t)a.K * (F32 ? 4 : 2);
   const bool full = nchunks == (int64_t)64 * W;
   auto kern = full ? k1_team<N0, F32, BITS, true> : k1_team<N0, F32, BITS, false>;
+  // the production path (bf16, N0 = 16, int8 codes) at the FLUX widths:
+  // compile-time team width (CRT_K1_WC=0 keeps the runtime-width kernel)
+  static const bool wc_off = [] {
+    const char* e = getenv("CRT_K1_WC");
+    return e && e[0] == '0';
+  }();
+  int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
+  if constexpr (N0 == 16 && !F32 && BITS == 5) {
+    if (full && !wc_off) {
+      if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
+      else if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
+      else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
+    }
+  }
   // ring depth: up to 4 stages while every CTA the registers allow still fits
   // in ~220 KB of shared memory per SM; at least 2
   int per_sm_r = 0;
@@ -399,8 +415,8 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   a.stages = S;
   const size_t smem = (size_t)S * rb;
   {
-    static SmemAttr attr[2];  // per instantiation, [full]
-    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[full], true);
+    static SmemAttr attr[5];  // per kernel: [runtime width, not full / full, W = 3 / 12 / 15]
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[ki], true);
     if (e != cudaSuccess) return e;
   }
   int per_sm = 0;

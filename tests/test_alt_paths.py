@@ -1,6 +1,7 @@
 """Opt-in kernel paths stay bit-exact: the mma.sync K1 (CRT_K1_MMA=1), the
 tcgen05 tensor-core K1 (CRT_K1_TC=1), the round-1 rolled K1 (CRT_K1_TEAM=0),
-the register-resident single-pass K1 (CRT_K1_FAST=1), the v1 single-CTA K3
+the register-resident single-pass K1 (CRT_K1_FAST=1), the runtime-width team
+K1 at the FLUX widths (CRT_K1_WC=0), the v1 single-CTA K3
 (CRT_K3_V1=1), the round-2 hardware-expansion W4A4 K3 (CRT_K3_V3=1), both
 v4 token-tile widths forced (CRT_K3_V4_BT=176 / 192), the
 TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-token I2F dequant
@@ -16,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{}, {"CRT_K1_MMA": "1"}, {"CRT_K1_FAST": "1"}, {"CRT_K1_TC": "1"},
-                                 {"CRT_K1_TEAM": "0"}, {"CRT_K3_V1": "1"},
+                                 {"CRT_K1_TEAM": "0"}, {"CRT_K1_WC": "0"}, {"CRT_K3_V1": "1"},
                                  {"CRT_K3_V3": "1"}, {"CRT_K3_V4_BT": "176"},
                                  {"CRT_K3_V4_BT": "192"}, {"CRT_K3_W8_TS": "1"},
                                  {"CRT_K3_NO_FDQ": "1"}])
