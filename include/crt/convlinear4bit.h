@@ -321,11 +321,11 @@ int64_t crt_launch_count(void);
  * K1 team kernel records %globaltimer stamps into it, 26 uint64 words per
  * CTA (kernel start, after the PDL wait, then per row: data ready, team
  * barrier passed, row done, for the first 8 rows).  NULL turns it off. */
-void crt_debug_k1_trace(void* buf);
+void crt_debug_k1_trace(void* buf);  /* effective in builds with -DCRT_K1_TRACE */
 /* Dev aid: K3 (v3) clock64 stamps of the first CTA pair's leader CTA into
  * buf (11 x 4096 uint64: per stage and per tile, see k3_gemm_v3.cu).  NULL
  * turns it off. */
-void crt_debug_k3_trace(void* buf);
+void crt_debug_k3_trace(void* buf);  /* effective in builds with -DCRT_K3_TRACE */
 int32_t crt_abi_version(void);
 
 #ifdef __cplusplus

@@ -291,7 +291,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     for (int gs = grp; gs < G; gs += 2) {
       const int s = gs % V4_PS, slot = gs % V4_SLOTS;
       mbar_wait(&ss->full[s], (uint32_t)(gs / V4_PS) & 1u);
+#ifdef CRT_K3_TRACE
       if (xtr && gs < kK3TraceN) xtr[xr * kK3TraceN + gs] = globaltimer();
+#endif
       const uint32_t src = smem_u32(stg + s * V4_STAGE) + (uint32_t)row * 64u;
       uint4 p[4];
 #pragma unroll
@@ -310,7 +312,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
+#ifdef CRT_K3_TRACE
       if (xtr && gs < kK3TraceN) xtr[(xr + 1) * kK3TraceN + gs] = globaltimer();
+#endif
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(slot_full0 + (uint32_t)slot * 8u)
                      : "memory");

@@ -174,8 +174,12 @@ __device__ __forceinline__ void lds_row32(uint32_t saddr, uint32_t (&v)[32]) {
 
 // dev-aid trace stamps (crt_debug_k3_trace): row x kK3TraceN clock64 words
 constexpr int kK3TraceN = 4096;
+// (compiled out unless built with -DCRT_K3_TRACE: the checks sit in the MMA
+// issuers' per-stage path)
 __device__ __forceinline__ void k3_stamp(unsigned long long* tr, int row, int i) {
+#ifdef CRT_K3_TRACE
   if (tr && i < kK3TraceN) tr[row * kK3TraceN + i] = clock64();
+#endif
 }
 
 }  // namespace

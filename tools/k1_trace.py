@@ -1,4 +1,6 @@
-"""Timeline of one K1 team-kernel launch from in-kernel %globaltimer stamps
+"""Needs a trace build: CRT_NVCC_EXTRA="-DCRT_K1_TRACE -DCRT_K3_TRACE" python -m
+paper_2512_03673_b200.build.
+Timeline of one K1 team-kernel launch from in-kernel %globaltimer stamps
 (crt_debug_k1_trace): per CTA, kernel start, PDL wait done, and for each of
 its rows the time the row's data was ready, the team barrier passed and the
 row finished.  python tools/k1_trace.py M K [N0]"""

@@ -1,4 +1,6 @@
-"""K3 v3 pipeline trace (crt_debug_k3_trace, 9 x 4096 words): clock64 stamps of pair 0's
+"""Needs a trace build: CRT_NVCC_EXTRA="-DCRT_K1_TRACE -DCRT_K3_TRACE" python -m
+paper_2512_03673_b200.build.
+K3 v3 pipeline trace (crt_debug_k3_trace, 9 x 4096 words): clock64 stamps of pair 0's
 leader CTA per stage (producer issue after the empty wait, MMA issue once
 the stage landed; two MMA threads take alternate stages) and per tile (MMA tile start,
 epilogue sees acc_full, epilogue done).  Prints the steady-state cycles per
