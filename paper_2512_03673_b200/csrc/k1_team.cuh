@@ -53,7 +53,8 @@ __device__ __forceinline__ uint32_t near_tie_mask_v(const float2 (&v)[16], float
 }
 
 // WC > 0: the team width as a compile-time constant (the FLUX widths of the
-// production instantiation), so the per-row team loops and index math fold.
+// production instantiation), so the per-row team loops and index math fold;
+// those instantiations also fix forward's outputs (PROD below).
 template <int N0, bool F32, int BITS, bool FULL, int WC = 0>
 __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
   constexpr int L = Stages<N0>::L;
@@ -76,6 +77,14 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
   const uint32_t row_bytes = (uint32_t)(a.K * esz);
   const int64_t row_step = gridDim.x;
   const bool t0 = threadIdx.x == 0;
+  // The compile-time-width instantiations serve only forward's K1 (launcher):
+  // codes, row sums and fp32 scales present, no caller max, no outlier max.
+  constexpr bool PROD = WC > 0;
+  const double* const amax_in = PROD ? nullptr : a.amax_in;
+  double* const amax_out = PROD ? nullptr : a.amax;
+  int32_t* const rowsum = a.rowsum;
+  const bool has_rowsum = PROD || rowsum != nullptr;
+  const bool has_codes = PROD || a.codes != nullptr;
 
 #ifdef CRT_K1_TRACE  // dev aid, compiled out by default (costs ~4%: fc2 53.4 vs 51.4 us)
   unsigned long long* trace = a.trace ? a.trace + (size_t)blockIdx.x * (2 + 3 * kK1TraceRows) : nullptr;
@@ -147,7 +156,7 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
     const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(max_nan(mx, my)));
     const float Aw = __uint_as_float(wm);
     double cmax = 0.0;
-    if (!a.amax_in) {
+    if (!amax_in) {
       if (!(Aw <= 3.0e38f)) {  // non-finite input / fp32 overflow: exact loop
         cmax = k1_slow_row_amax<F32>(rowp, 2, W, w, nchunks, a.group, a.kind, a.rot_cols);
       } else if (N0 == 1) {
@@ -230,14 +239,14 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
         }
       }
     }
-    if (a.rowsum && prev >= 0 && w == (W > 1 ? 1 : 0)) {
+    if (has_rowsum && prev >= 0 && w == (W > 1 ? 1 : 0)) {
       const int sum = __reduce_add_sync(0xffffffffu, lane < W ? s_sum[par ^ 1][lane] : 0);
-      if (lane == 0) a.rowsum[prev] = sum;
+      if (lane == 0) rowsum[prev] = sum;
     }
     const float A32 = __uint_as_float(
         __reduce_max_sync(0xffffffffu, lane < W ? s_amax[par][lane] : 0u));
     const double amax_ref =
-        a.amax_in ? a.amax_in[row] : warp_max_d(lane < W ? s_cmax[par][lane] : 0.0);
+        amax_in ? amax_in[row] : warp_max_d(lane < W ? s_cmax[par][lane] : 0.0);
     const bool slow_row = !(A32 <= 3.0e38f);  // uniform over the team
     const bool invalid = !isfinite(amax_ref);
     // s = amax/QMAX in double (quant.cpp:21) is needed only by thread 0 (the
@@ -248,15 +257,15 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
     if (t0) {
       const double s = scale();
       if (invalid) flag_invalid_value(a.err);
-      if (a.s32) a.s32[row] = (float)s;
+      if (PROD || a.s32) a.s32[row] = (float)s;
       if (a.s64) a.s64[row] = s;
-      if (a.amax) a.amax[row] = amax_ref;  // exact max|y_ref| (outlier analysis)
+      if (amax_out) amax_out[row] = amax_ref;  // exact max|y_ref| (outlier analysis)
     }
 
     // ---- certified quantisation + pack + store from registers --------------
     uint8_t* crow = a.codes + row * a.ldc;
     int csum = 0;
-    if (!a.codes) {
+    if (!has_codes) {
       // amax only (crt_rotated_row_absmax): no codes
     } else if (!slow_row) {
       // inv = rk*QMAX/amax from an fp32 reciprocal (within 3 ulp of rk/s,
@@ -345,7 +354,7 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
       if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
     }
     if constexpr (BITS == 5) {
-      if (a.rowsum) {
+      if (has_rowsum) {
         const int ws = __reduce_add_sync(0xffffffffu, csum);
         if (lane == 0) s_sum[par][w] = ws;
       }
@@ -360,12 +369,12 @@ __global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
       phase ^= 1u;
     }
   }
-  if (a.rowsum && prev >= 0) {
+  if (has_rowsum && prev >= 0) {
     __syncthreads();
     if (t0) {
       int sum = 0;
       for (int i = 0; i < W; ++i) sum += s_sum[par ^ 1][i];
-      a.rowsum[prev] = sum;
+      rowsum[prev] = sum;
     }
   }
 }
@@ -403,7 +412,7 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   }();
   int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
   if constexpr (N0 == 16 && !F32 && BITS == 5) {
-    if (full && !wc_off) {
+    if (full && !wc_off && a.codes && a.rowsum && a.s32 && !a.amax_in && !a.amax) {
       if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
       else if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
       else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
