@@ -411,11 +411,13 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
     return e && e[0] == '0';
   }();
   int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
-  if constexpr (N0 == 16 && !F32 && BITS == 5) {
+  if constexpr (!F32 && BITS == 5) {
     if (full && !wc_off && a.codes && a.rowsum && a.s32 && !a.amax_in && !a.amax) {
-      if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
-      else if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
-      else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
+      if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;  // K = 3072, every N0 (cfg1-3)
+      if constexpr (N0 == 16) {  // the FLUX MLP / proj_out widths
+        if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
+        else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
+      }
     }
   }
   // ring depth: up to 4 stages while every CTA the registers allow still fits
