@@ -84,6 +84,19 @@ template <int BT>
 __device__ __forceinline__ uint32_t a_col(int s) {
   return (s < 2 ? (uint32_t)BT : 256u + (uint32_t)BT) + (uint32_t)(s & 1) * 32u;
 }
+// Epilogue output staging (YT): one 32-token x 32-channel bf16 box (2 KB)
+// per epilogue warp, written with st.shared and stored by one TMA bulk
+// tensor store; the tensor map clips tokens >= M and channels >= N.
+constexpr int V4_YSTG = 2048;
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t saddr, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   map),
+               "r"(x), "r"(y), "r"(saddr)
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -150,14 +163,17 @@ struct V4Args {
   int64_t ldy;
   int32_t fdq;       // magic-number fp32x2 dequant (bf16 output)
   unsigned long long* trace;  // dev aid (crt_debug_k3_trace), as v3's layout
-  int32_t dbg;                // dev aid (CRT_K3_V4_DBG bitmask, timing only, wrong output):
+  int32_t dbg;                // dev aid (builds with -DCRT_K3_DBG; CRT_K3_V4_DBG bitmask, timing only, wrong output):
                               // 1 no A-slot stores, 2 no dequant/stores, 4 no TMEM loads/zeroing
 };
 
-template <int BT>
+// YT: bf16 output through shared-memory boxes and TMA bulk stores (set by
+// the launcher when out_kind == bf16 and y is 16-byte aligned).
+template <int BT, bool YT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     k3_v4_kernel(const __grid_constant__ CUtensorMap map_w,
-                 const __grid_constant__ CUtensorMap map_x, V4Args a) {
+                 const __grid_constant__ CUtensorMap map_x,
+                 const __grid_constant__ CUtensorMap map_y, V4Args a) {
   using C = V4Cfg<BT>;
   constexpr int V4_BT = BT, V4_BTH = C::BTH, V4_B = C::B, V4_STAGE = C::STAGE, V4_SLOTS = C::SLOTS;
   using V4Smem = crt::V4Smem<BT>;
@@ -165,6 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = smem;                          // V4_PS x (packed A 8 KB | B 12 KB)
   V4Smem* ss = reinterpret_cast<V4Smem*>(smem + V4_PS * V4_STAGE);
+  uint8_t* ystg = smem + V4_PS * V4_STAGE + ((sizeof(V4Smem) + 127) & ~(size_t)127);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -204,6 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    if (YT) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_y) : "memory");
   }
   griddep_launch();
   griddep_wait();
@@ -308,7 +326,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
       }
       mbar_wait(&ss->slot_empty[slot], ((uint32_t)(gs / V4_SLOTS) & 1u) ^ 1u);
       tc_fence_after();
-      if (!(a.dbg & 1)) tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col<BT>(slot), o);
+#ifdef CRT_K3_DBG
+      if (!(a.dbg & 1))
+#endif
+        tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + a_col<BT>(slot), o);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -323,6 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     // ===== epilogue (v3's): TMEM -> dequant -> direct stores ===============
     const int q = warp & 3;
     const int et = threadIdx.x - 128;  // 0 .. V4_EPI_THREADS-1
+    const uint32_t ybuf = smem_u32(ystg) + (uint32_t)(warp - 4) * V4_YSTG;
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
     // fdq: acc + (0x4B400000 - 8 S_a) are the float bits of 1.5*2^23 + v,
     // exact while |v| < 2^22 (|v| <= 49 K: K <= 85598)
@@ -367,9 +389,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
         uint32_t acc[32];
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc_col(ab) + c * 32;
         const int cw = (C::LASTW == 32 || c < C::NCH - 1) ? 32 : 16;  // chunk width
-        if (a.dbg & 4) {
-          continue;
-        } else if (cw == 32) {
+#ifdef CRT_K3_DBG
+        if (a.dbg & 4) continue;
+#endif
+        if (cw == 32) {
           tmem_ld32(ta, acc);
           tmem_zero32(ta);
         } else {
@@ -377,10 +400,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
           tmem_zero16(ta);
         }
         const int64_t m0 = mb + c * 32;
-        if (m0 >= a.M || !nok || (a.dbg & 2)) continue;
-        const int jn = a.M - m0 < cw ? (int)(a.M - m0) : cw;
+#ifdef CRT_K3_DBG
+        if (a.dbg & 2) continue;
+#endif
         const int* sm = &ss->sums[c * 32];
         const float* sa = &ss->sa[c * 32];
+        if constexpr (YT) {
+          if (cw == 32) {
+            // the whole 32 x 32 box through shared memory and one TMA store;
+            // tokens >= M and channels >= N are clipped by the tensor map
+            if (m0 >= a.M || nw >= a.N) continue;
+            uint32_t sav[32], smv[32];
+            lds_row32(smem_u32(sa), sav);
+            lds_row32(smem_u32(sm), smv);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();  // the previous box has left the buffer
+            if (fdq) {
+              const float2 mc = make_float2(-12582912.f, -12582912.f);  // -1.5 * 2^23
+              const float2 w2 = make_float2(sw, sw), b2 = make_float2(bn, bn);
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const float2 mm = make_float2(__uint_as_float(acc[j] + smv[j]),
+                                              __uint_as_float(acc[j + 1] + smv[j + 1]));
+                const float2 v = __fadd2_rn(mm, mc);
+                const float2 p =
+                    __fmul2_rn(v, make_float2(__uint_as_float(sav[j]), __uint_as_float(sav[j + 1])));
+                const __nv_bfloat162 o = __float22bfloat162_rn(__ffma2_rn(p, w2, b2));
+                st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o.x));
+                st_shared_u16(ybuf + (uint32_t)(j + 1) * 64u + (uint32_t)lane * 2u,
+                              __bfloat16_as_ushort(o.y));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int v = (int)acc[j] - (int)smv[j];
+                const __nv_bfloat16 o =
+                    __float2bfloat16_rn(fmaf((float)v * __uint_as_float(sav[j]), sw, bn));
+                st_shared_u16(ybuf + (uint32_t)j * 64u + (uint32_t)lane * 2u, __bfloat16_as_ushort(o));
+              }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_y, ybuf, (int)nw, (int)m0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            continue;
+          }
+        }
+        if (m0 >= a.M || !nok) continue;
+        const int jn = a.M - m0 < cw ? (int)(a.M - m0) : cw;
         if (a.out_kind == 0) {
           __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(a.y) + m0 * a.ldy + n;
           if (jn == 32) {
@@ -438,6 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
         aph ^= 1;
       }
     }
+    if (YT && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // boxes written
   }
 
   tc_fence_before();
@@ -474,6 +544,10 @@ bool k3_v4_supported(const K3Args& a) {
 namespace {
 template <int BT>
 cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int num_sms) {
+  static const bool ydirect = [] {  // A/B: per-lane global stores instead of TMA boxes
+    const char* e = getenv("CRT_K3_V4_YDIRECT");
+    return e && e[0] == '1';
+  }();
   using C = V4Cfg<BT>;
   auto fn = encode_fn_v4();
   CUtensorMap mw, mx;
@@ -521,17 +595,32 @@ cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int n
     return e ? atoi(e) : 0;
   }();
   v.dbg = dbg;
-  const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127);
-  static SmemAttr attr;
+  // bf16 output map for the TMA-store epilogue: N channels (inner) x M tokens, 32 x 32 boxes
+  CUtensorMap my = mx;
+  bool yt = false;
+  if (a.out_kind == 0 && !ydirect && (uintptr_t)a.y % 16 == 0 && (a.ldy * 2) % 16 == 0) {
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)(a.ldy * 2)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    yt = fn(&my, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.y, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (!yt) my = mx;
+  }
+  auto kern = yt ? k3_v4_kernel<BT, true> : k3_v4_kernel<BT, false>;
+  const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127) +
+                      (yt ? V4_EPI_WARPS * V4_YSTG : 0);
+  static SmemAttr attr[2];
   {
-    const cudaError_t e = ensure_dyn_smem(k3_v4_kernel<BT>, smem, attr, false);
+    const cudaError_t e = ensure_dyn_smem(kern, smem, attr[yt], false);
     if (e != cudaSuccess) return e;
   }
   const int tiles = v.ttiles * v.ctiles;
   int pairs = num_sms / 2;
   if (pairs > tiles) pairs = tiles;
-  const cudaError_t le = launch_pdl(k3_v4_kernel<BT>, dim3((unsigned)(2 * pairs)),
-                                    dim3(V4_THREADS), smem, st, mw, mx, v);
+  const cudaError_t le = launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(V4_THREADS), smem, st,
+                                    mw, mx, my, v);
   ++*launches;
   return le;
 }
