@@ -54,9 +54,12 @@ __device__ __forceinline__ uint32_t near_tie_mask_v(const float2 (&v)[16], float
 
 // WC > 0: the team width as a compile-time constant (the FLUX widths of the
 // production instantiation), so the per-row team loops and index math fold;
-// those instantiations also fix forward's outputs (PROD below).
+// those instantiations also fix forward's outputs (PROD below).  W = 15 runs
+// one CTA per SM whatever its registers, so it gets up to 128 (74.8 vs 78.1
+// us at K = 15360: fewer rematerialisations); 3 and 12 keep 80 (8 and 2
+// CTAs per SM).
 template <int N0, bool F32, int BITS, bool FULL, int WC = 0>
-__global__ void __maxnreg__(kK1TRegs) k1_team(K1Args a) {
+__global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
   constexpr int L = Stages<N0>::L;
   constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
   griddep_launch();
