@@ -344,7 +344,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
     // ===== epilogue (v3's): TMEM -> dequant -> direct stores ===============
     const int q = warp & 3;
     const int et = threadIdx.x - 128;  // 0 .. V4_EPI_THREADS-1
-    const uint32_t ybuf = smem_u32(ystg) + (uint32_t)(warp - 4) * V4_YSTG;
+    // two boxes per warp: a chunk's st.shared overlaps the previous box's TMA read
+    const uint32_t ybuf0 = smem_u32(ystg) + (uint32_t)(warp - 4) * 2u * V4_YSTG;
+    uint32_t ysel = 0;
     const uint32_t empty_acc = mapa(smem_u32(&ss->acc_empty[0]), 0);
     // fdq: acc + (0x4B400000 - 8 S_a) are the float bits of 1.5*2^23 + v,
     // exact while |v| < 2^22 (|v| <= 49 K: K <= 85598)
@@ -413,8 +415,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V4_THREADS, 1)
             uint32_t sav[32], smv[32];
             lds_row32(smem_u32(sa), sav);
             lds_row32(smem_u32(sm), smv);
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();  // the previous box has left the buffer
+            const uint32_t ybuf = ybuf0 + ysel * V4_YSTG;
+            ysel ^= 1u;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();  // the box stored two chunks ago has left this buffer
             if (fdq) {
               const float2 mc = make_float2(-12582912.f, -12582912.f);  // -1.5 * 2^23
               const float2 w2 = make_float2(sw, sw), b2 = make_float2(bn, bn);
@@ -610,7 +614,7 @@ cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int n
   }
   auto kern = yt ? k3_v4_kernel<BT, true> : k3_v4_kernel<BT, false>;
   const size_t smem = 1024 + V4_PS * C::STAGE + ((sizeof(V4Smem<BT>) + 127) & ~(size_t)127) +
-                      (yt ? V4_EPI_WARPS * V4_YSTG : 0);
+                      (yt ? 2 * V4_EPI_WARPS * V4_YSTG : 0);
   static SmemAttr attr[2];
   {
     const cudaError_t e = ensure_dyn_smem(kern, smem, attr[yt], false);

@@ -22,6 +22,7 @@ for (M, K, N, n0) in [(96, 3072, 384, 16), (40, 1536, 256, 256), (33, 1040, 160,
         q = QuantSpec(bits)
         layer = crt.prepare_layer(w, None, spec, q)
         y = crt.forward(x, layer, q, out="f32")
+        crt.forward(x, layer, q)  # bf16: K3 v4's TMA-store epilogue
         codes, s = crt.rotate_quantize(x, spec, q)
         if bits == 4:
             crt.rotate_quantize_i8(x, spec)
