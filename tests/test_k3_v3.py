@@ -1,6 +1,7 @@
-"""K3 v3 (weights expanded by tcgen05.cp decompression, int8 activation codes
-from K1's bits-5 mode) against the exact integer GEMM of the same codes and
-against the packed v2 path.  The int_gemm accumulators must be bit-exact
+"""The int8-activation-code K3 (v4 by default: packed weights expanded by
+expander warps into tensor memory; v3 with CRT_K3_V3=1, re-run by
+tests/test_alt_paths.py: tcgen05.cp decompression) against the exact
+integer GEMM of the same codes and against the packed v2 path.  The int_gemm accumulators must be bit-exact
 (pipeline.cpp:178-204) and the dequantised outputs identical to v2's, which
 tests/test_gpu_parity.py pins to the oracle.  Shapes cover ragged token tiles
 (M not a multiple of 192), ragged channel tiles (N not a multiple of 256),
