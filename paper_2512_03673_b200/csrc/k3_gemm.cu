@@ -430,6 +430,7 @@ cudaError_t k3_launch(const K3Args& a, cudaStream_t st, int64_t* launches) {
     return e && e[0] == '1';
   }();
   if (a.a_layout == 1) {  // int8-stored 4-bit activation codes: v4 (default) or v3
+    if (!force_v3 && k3_gemv_supported(a)) return k3_gemv_launch(a, st, launches);
     if (!force_v3 && k3_v4_supported(a)) return k3_v4_launch(a, st, launches);
     if (k3_v3_supported(a)) return k3_v3_launch(a, st, launches);
     return cudaErrorInvalidValue;

@@ -69,6 +69,10 @@ cudaError_t k3_v3_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 bool k3_v4_supported(const K3Args& a);
 cudaError_t k3_v4_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 int k3_v4_pick_bt(int64_t M, int64_t N, int num_sms);  // token-tile width v4 uses
+// M <= 8 (FLUX AdaLN): a weight-streaming CUDA-core GEMV on the same operands
+// (k3_gemv.cu); CRT_K3_GEMV=0 keeps the tensor-core kernel.
+bool k3_gemv_supported(const K3Args& a);
+cudaError_t k3_gemv_launch(const K3Args& a, cudaStream_t st, int64_t* launches);
 // Dev aid (crt_debug_k3_trace): when set, k3_v3 records clock64 stamps of
 // pair 0's leader CTA (9 rows x 4096, see k3_gemm_v3.cu); null = off.
 void set_k3_trace(unsigned long long* buf);

@@ -21,7 +21,7 @@ def main():
     y16_hash = hashlib.md5()
     for n0 in (4, 16):
         for fam in ("gaussian", "colwise", "rowwise"):
-            for (m, k, n) in ((97, 3072, 80), (40, 12288, 48)):
+            for (m, k, n) in ((97, 3072, 80), (40, 12288, 48), (5, 3072, 80)):
                 xb = O.synth_input(m, k, fam, 3 + n0)
                 wb = O.synth_input(n, k, "gaussian", 4 + n0)
                 x, w = to_t(xb), to_t(wb)

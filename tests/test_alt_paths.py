@@ -4,7 +4,8 @@ the register-resident single-pass K1 (CRT_K1_FAST=1), the runtime-width team
 K1 at the FLUX widths (CRT_K1_WC=0), the v1 single-CTA K3
 (CRT_K3_V1=1), the round-2 hardware-expansion W4A4 K3 (CRT_K3_V3=1), both
 v4 token-tile widths forced (CRT_K3_V4_BT=176 / 192), the v4 per-lane store
-epilogue (CRT_K3_V4_YDIRECT=1), the
+epilogue (CRT_K3_V4_YDIRECT=1), the tensor-core kernel at M <= 8
+(CRT_K3_GEMV=0), the
 TMEM-copy W8A8 K3 (CRT_K3_W8_TS=1) and the per-token I2F dequant
 (CRT_K3_NO_FDQ=1), each -- and the defaults -- in a fresh process."""
 import os
@@ -21,6 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                  {"CRT_K1_TEAM": "0"}, {"CRT_K1_WC": "0"}, {"CRT_K3_V1": "1"},
                                  {"CRT_K3_V3": "1"}, {"CRT_K3_V4_BT": "176"},
                                  {"CRT_K3_V4_BT": "192"}, {"CRT_K3_V4_YDIRECT": "1"},
+                                 {"CRT_K3_GEMV": "0"},
                                  {"CRT_K3_W8_TS": "1"},
                                  {"CRT_K3_NO_FDQ": "1"}])
 def test_opt_in_paths_bit_exact(env):
