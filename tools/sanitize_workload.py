@@ -14,7 +14,8 @@ from paper_2512_03673_b200 import QuantSpec, RotationKind, RotationSpec  # noqa:
 
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(3)
-for (M, K, N, n0) in [(96, 3072, 384, 16), (40, 1536, 256, 256), (33, 1040, 160, 16)]:
+for (M, K, N, n0) in [(96, 3072, 384, 16), (40, 1536, 256, 256), (33, 1040, 160, 16),
+                      (3, 3072, 200, 16)]:  # M <= 8: the K3 GEMV
     x = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
     w = torch.randn(N, K, device=dev, generator=g).to(torch.bfloat16)
     spec = RotationSpec(RotationKind.regular, n0)

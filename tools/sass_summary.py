@@ -23,7 +23,7 @@ for line in out.splitlines():
         kern = ("k1_team" if "k1_team" in name else "k1_rolled" if "k1_rolled" in name else
                 "k1_fast" if "k1_fast" in name else "k1_exact" if "k1_exact" in name else
                 "k1_mma" if "k1_mma" in name else "k3_v3" if "k3_v3" in name else
-                "k3_v4" if "k3_v4" in name else
+                "k3_v4" if "k3_v4" in name else "k3_gemv" if "k3_gemv" in name else
                 "k3_v2" if "k3_v2" in name else "k3_ss (v1)" if "k3_ss" in name else
                 "other")
         fam[kern]["#functions"] += 1
