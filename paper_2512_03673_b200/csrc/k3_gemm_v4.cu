@@ -602,7 +602,10 @@ cudaError_t launch_bt(const K3Args& a, cudaStream_t st, int64_t* launches, int n
   // bf16 output map for the TMA-store epilogue: N channels (inner) x M tokens, 32 x 32 boxes
   CUtensorMap my = mx;
   bool yt = false;
-  if (a.out_kind == 0 && !ydirect && (uintptr_t)a.y % 16 == 0 && (a.ldy * 2) % 16 == 0) {
+  // (the TMA store clips at N in 16-byte units: with N % 8 != 0 it would
+  // write up to 7 columns past N, which a caller's wider row may own)
+  if (a.out_kind == 0 && !ydirect && (uintptr_t)a.y % 16 == 0 && (a.ldy * 2) % 16 == 0 &&
+      a.N % 8 == 0) {
     cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
     cuuint64_t strides[1] = {(cuuint64_t)(a.ldy * 2)};
     cuuint32_t box[2] = {32, 32};

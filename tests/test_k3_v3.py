@@ -95,3 +95,29 @@ def test_v3_w8a8_accumulators_exact(M, K, N):
         assert torch.equal(crt.quant_gemm(codes, sa, layer, q8, out=out),
                            crt.dequant(acc, sa, layer, out=out)), out
     assert torch.equal(crt.forward(x, layer, q8, out="i32"), acc)
+
+
+@pytest.mark.parametrize("M,K,N,ldy", [(300, 3072, 1000, 1024), (257, 3104, 700, 712), (5, 3072, 300, 320),
+                                       (193, 1536, 40, 48)])
+@pytest.mark.parametrize("out", ["bf16", "f32"])
+def test_forward_into_wider_rows(M, K, N, ldy, out):
+    """y as a column block of a wider row-major buffer (ldy > N): the K3
+    epilogue (v4's TMA-store boxes clip at N through the tensor map; the GEMV
+    and the per-lane stores index with ldy) must write exactly the [M, N]
+    block, leave the columns beyond N untouched, and equal the contiguous
+    forward."""
+    import paper_2512_03673_b200 as crt
+    from paper_2512_03673_b200 import RotationKind, RotationSpec
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(M + N)
+    x = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+    w = torch.randn(N, K, device=dev, generator=g).to(torch.bfloat16)
+    b = torch.randn(N, device=dev, generator=g)
+    layer = crt.prepare_layer(w, b, RotationSpec(RotationKind.regular, 16))
+    ref = crt.forward(x, layer, out=out)
+    dt = torch.bfloat16 if out == "bf16" else torch.float32
+    big = torch.full((M, ldy), 7.0, dtype=dt, device=dev)
+    crt.forward(x, layer, out=out, y=big[:, :N])
+    torch.cuda.synchronize()
+    assert torch.equal(big[:, :N], ref)
+    assert bool((big[:, N:] == 7.0).all())
