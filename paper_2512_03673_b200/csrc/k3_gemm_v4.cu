@@ -42,7 +42,10 @@ namespace crt {
 namespace {
 
 constexpr int V4_BM = 128;         // channels per CTA (pair: 256)
-constexpr int V4_PS = 10;          // stages
+#ifndef CRT_K3_V4_PS
+#define CRT_K3_V4_PS 10
+#endif
+constexpr int V4_PS = CRT_K3_V4_PS;  // stages
 constexpr int V4_EPI_WARPS = 4;    // epilogue warps 4..7 (one per TMEM lane quarter)
 constexpr int V4_EXP_WARPS = 8;    // expander warps per CTA: 3 and 8..14, two groups of 4
 constexpr int V4_THREADS = 32 * (4 + V4_EPI_WARPS + V4_EXP_WARPS - 1);
