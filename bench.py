@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--path", choices=["v3", "v2"], default="v3",
-                    help="K1+K3 pair: v3 (int8 codes, hardware weight expansion; what "
-                         "forward() runs) or v2 (packed codes, software expansion)")
+                    help="K1+K3 pair: v3 (int8 activation codes -> K3 v4, or K3 v3 under "
+                         "CRT_K3_V3=1; what forward() runs) or v2 (packed codes, "
+                         "software expansion)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config blocks (cfg1, cfg3 N0 sweep, cfg4 FLUX stack)")
     ap.add_argument("--cpu-stages", type=int, default=0, metavar="ROWS",
@@ -778,7 +779,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "int4",
             "data": "synthetic (seeded gaussian bf16 activations, random-init weights)",
             "config": {"workload": WORKLOAD, "M": M_TOK, "d_model": D_MODEL, "d_ff": D_FF,
-                       "n0": n0, "bits": "W4A4", "k3_path": args.path,
+                       "n0": n0, "bits": "W4A4", "k3_path": ("int8 activation codes (K1 team -> K3 v4)" if v3 and
+                                   os.environ.get("CRT_K3_V3") != "1" else args.path),
                        "parallelism": (
                            f"fc1 column-parallel (no gather) -> fc2 row-parallel (int32 SUM "
                            f"all-reduce) x{world}, C-ABI crt_tp_* over NCCL"
@@ -788,10 +790,14 @@ def run_ours(args):
                            f"prompt replicas x{world}" if world > 1 else "single"),
                        "l2": "flushed (256 MiB write) between steps, outside the timed events"},
             "roofline": {"bound": "tensor",
-                         "kernel": ("per-rank tensor-parallel layer forward (K1 + K3 v3 + NCCL); "
+                         "kernel": ("per-rank tensor-parallel layer forward (K1 + K3 + NCCL); "
                                     "the ops are this rank's share" if column else
                                     "k3_v3_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, weights "
-                                    "expanded by tcgen05.cp decompression)") if v3 else
+                                    "expanded by tcgen05.cp decompression; CRT_K3_V3=1)"
+                                    if os.environ.get("CRT_K3_V3") == "1" else
+                                    "k3_v4_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, packed "
+                                    "weights TMA-staged, expanded into TMEM A by tcgen05.st)")
+                                   if v3 else
                                    "k3_v2_kernel (W4A4 GEMM, 2-SM tcgen05 kind::i8, TMEM-A)",
                          "achieved": k3_tops, "peak": int8_peak, "unit": "TFLOP/s",
                          "frac": k3_tops / int8_peak, "traffic": traffic,
