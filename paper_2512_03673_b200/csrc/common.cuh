@@ -68,6 +68,13 @@ __device__ __forceinline__ void ld_nc_v8(const void* p, uint32_t (&v)[8]) {
       : "l"(p));
 }
 
+// 256-bit store (STG.E.ENL2.256): 8 words at a 32-byte aligned address.
+__device__ __forceinline__ void st_v8(void* p, uint4 lo, uint4 hi) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(lo.x), "r"(lo.y),
+               "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -52,6 +52,157 @@ __device__ __forceinline__ uint32_t near_tie_mask_v(const float2 (&v)[16], float
   return fm;
 }
 
+// The reference's element-by-element max / codes over the calling lane's
+// chunk pair (c0, c0 + cstride): rows the fp32 path cannot certify
+// (non-finite input, fp32 overflow) in the lane-pair layout (XG below).
+// Same arithmetic as k1_slow_row_*.
+template <bool F32>
+__device__ __noinline__ double k1_slow_pair_amax(const void* rowp, int64_t c0, int64_t cstride,
+                                                 int64_t nchunks, int64_t group, int kind,
+                                                 int64_t rot_cols) {
+  double m = 0.0;
+  bool bad = false;
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0 + h * cstride;
+    if (chunk >= nchunks) continue;
+    for (int i = 0; i < 16; ++i) {
+      const double yr = y_ref<F32>(rowp, chunk * 16 + i, group, kind, rot_cols);
+      if (!isfinite(yr)) bad = true;
+      m = fmax(m, fabs(yr));
+    }
+  }
+  return bad ? INFINITY : m;
+}
+
+template <bool F32, int BITS>
+__device__ __noinline__ void k1_slow_pair_codes(const void* rowp, uint8_t* crow, int64_t c0,
+                                                int64_t cstride, int64_t nchunks, bool invalid,
+                                                double s, int64_t group, int kind,
+                                                int64_t rot_cols) {
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0 + h * cstride;
+    if (chunk >= nchunks) continue;
+    for (int i = 0; i < 16; i += 2) {
+      int q0 = 0, q1 = 0;
+      if (!invalid) {
+        q0 = exact_code(y_ref<F32>(rowp, chunk * 16 + i, group, kind, rot_cols), s, QMAX);
+        q1 = exact_code(y_ref<F32>(rowp, chunk * 16 + i + 1, group, kind, rot_cols), s, QMAX);
+      }
+      if constexpr (BITS == 4) {
+        crow[chunk * 8 + i / 2] = (uint8_t)((q0 & 0x0F) | ((q1 & 0x0F) << 4));
+      } else {
+        crow[chunk * 16 + i] = (uint8_t)q0;
+        crow[chunk * 16 + i + 1] = (uint8_t)q1;
+      }
+    }
+  }
+}
+
+// Exponent-span certificate of a whole lane-pair-layout group (chunk_certified_bf16's
+// test): the calling lane's input chunks c0i, c0i + csi, combined over the
+// group's lanes (rotate_team's layout: lane bit 0 for N0 = 64, bits 0-2 for
+// 256) as packed 16-bit maxima of (max |x|, 0xFFFF - (min |x| - 1)).  True =>
+// every fp32 partial sum of the group's butterflies is exact.  Warp-uniform
+// call (shuffles).
+template <int N0>
+__device__ __forceinline__ bool group_certified_bf16(const void* rowp, int64_t c0i, int64_t csi) {
+  const uint32_t sa = smem_u32(rowp);
+  uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t ca = sa + (uint32_t)(c0i + h * csi) * 32u;
+    const uint4 t0 = ld_shared_v4(ca), t1 = ld_shared_v4(ca + 16);
+    const uint32_t u[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m = u[i] & 0x7FFF7FFFu;
+      mx = __vmaxu2(mx, m);
+      mn = __vminu2(mn, __vsub2(m, 0x00010001u));  // zeros -> 0xFFFF
+    }
+  }
+  const uint32_t bmx = max(mx & 0xFFFFu, mx >> 16);
+  const uint32_t bmn = min(mn & 0xFFFFu, mn >> 16);
+  uint32_t q = (bmx << 16) | (0xFFFFu - bmn);
+  q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 1));
+  if constexpr (N0 >= 256) {
+    q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 2));
+    q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 4));
+  }
+  const uint32_t bmax = q >> 16;
+  const uint32_t bmin = (0xFFFFu - (q & 0xFFFFu)) + 1u;  // 0x10000: all zero
+  if (bmax == 0u) return true;                          // all-zero group: y = 0
+  if (bmax >= 0x7F80u || bmin < 0x0080u) return false;  // inf/NaN or subnormal
+  constexpr int L2 = N0 == 64 ? 6 : 8;
+  return 1 + L2 + (int)((bmax >> 7) - (bmin >> 7)) + 8 <= 24;
+}
+
+// rotate_team's input chunks in the lane-pair layout (bf16 rows in shared memory): the
+// lane pairs' chunks sit at 128-byte-periodic offsets {0, 32}, so the two
+// 16-byte halves are read in an order alternating with lane bit 1 (2-way
+// instead of 4-way bank conflicts, like load_pair's consecutive chunks).
+template <bool FULL>
+__device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, int64_t c0i,
+                                             int64_t csi, int64_t nchunks, int lane) {
+  const uint32_t sw = (uint32_t)(lane >> 1) & 1u;
+  const uint32_t sb = smem_u32(rowp);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t chunk = c0i + h * csi;
+    uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
+    if (FULL || chunk < nchunks) {
+      const uint32_t ca = sb + (uint32_t)chunk * 32u;
+      const uint4 ta = ld_shared_v4(ca + 16u * sw), tb = ld_shared_v4(ca + 16u * (sw ^ 1u));
+      lo = sw ? tb : ta;
+      hi = sw ? ta : tb;
+    }
+    const uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float f = __uint_as_float((i & 1) ? (u[i >> 1] & 0xFFFF0000u) : (u[i >> 1] << 16));
+      if (h == 0) v[i].x = f;
+      else v[i].y = f;
+    }
+  }
+}
+
+// The team's rotation.  !XG: rotate_pair (in-chunk butterflies, outer
+// digits by xlane4).  XG (the lane-pair layout, N0 >= 64): the third radix-4 digit (element bits 4-5, the chunk's position
+// in its 4-chunk block) is split over the lane pair (lane, lane ^ 1): with
+// H4 = J - 2 antidiag = diag(1,1,1,-1) (H2 (x) H2) P, P the signed
+// permutation x -> (x0, x2, x1, -x3), lane a = lane & 1 loads INPUT chunks
+// {a, a + 2} of the block and holds OUTPUT chunks {2a, 2a + 1} (c0i / c0
+// in k1_team), so the digit is one in-register H2 plus one shuffled H2: 2 shuffles
+// and 4 FFMA per element pair instead of xlane4's 6 shuffles and 6 FADD/FFMA.
+// Each output takes two roundings (xlane4: three) with partial sums of the
+// same four terms, inside the error bound B.  N0 = 256
+// adds the fourth digit across lane bits 1-2 (xlane4, stride 2).
+template <int N0, bool XG>
+__device__ __forceinline__ void rotate_team(float2 (&v)[16], int lane) {
+  if constexpr (!XG) {
+    rotate_pair<N0>(v);
+  } else {
+    rotate_pair<16>(v);
+    const float sa = (lane & 1) ? -1.f : 1.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float ux = fmaf(v[i].y, sa, v[i].x);   // a = 0: x + y   a = 1: x - y
+      const float uy = fmaf(v[i].y, -sa, v[i].x);  //        x - y          x + y
+      const float px = __shfl_xor_sync(0xffffffffu, ux, 1);
+      const float py = __shfl_xor_sync(0xffffffffu, uy, 1);
+      v[i].x = fmaf(ux, sa, px);  // a = 0: u0 + u1 (y0)   a = 1: u0 - u1 (y2)
+      v[i].y = fmaf(py, sa, uy);  //        u0 + u1 (y1)          u1 - u0 (y3)
+    }
+    if constexpr (N0 >= 256) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        v[i].x = xlane4(v[i].x, 2);
+        v[i].y = xlane4(v[i].y, 2);
+      }
+    }
+  }
+}
+
 // WC > 0: the team width as a compile-time constant (the FLUX widths of the
 // production instantiation), so the per-row team loops and index math fold;
 // those instantiations also fix forward's outputs (PROD below).  W = 15 runs
@@ -73,8 +224,17 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.K / 16;
-  const int64_t cstride = (int64_t)W * 32;
-  const int64_t c0 = (int64_t)w * 32 + lane;  // my chunks: c0 and c0 + cstride
+  // my (output) chunks c0 and c0 + cstride; inputs c0i and c0i + csi.  The
+  // lane-pair layout (rotate_team) is chosen per instantiation as measured:
+  // N0 = 64 always (26.3 vs 28.1 us at M = 4608, K = 3072; 92.9 vs 105.8 at
+  // K = 12288); N0 = 256 in the runtime-width kernel (148 vs 155 us at K =
+  // 12288) but not at the folded W = 3, where it spills (43.4 vs 41.4 us).
+  constexpr bool XG = N0 == 64 || (N0 == 256 && WC == 0);
+  const int64_t gl = (int64_t)w * 32 + lane;
+  const int64_t cstride = XG ? 1 : (int64_t)W * 32;
+  const int64_t c0 = XG ? 4 * (gl >> 1) + 2 * (lane & 1) : gl;
+  const int64_t csi = XG ? 2 : cstride;
+  const int64_t c0i = XG ? 4 * (gl >> 1) + (lane & 1) : c0;
   const int esz = F32 ? 4 : 2;
   const int S = a.stages;
   const uint32_t row_bytes = (uint32_t)(a.K * esz);
@@ -147,8 +307,9 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
 
     // ---- load + rotate once; per-chunk |y| maxima ---------------------------
     float2 v[16];
-    load_pair<F32, true, FULL>(v, rowp, c0, cstride, nchunks);
-    rotate_pair<N0>(v);
+    if constexpr (XG && !F32) load_pair_xg<FULL>(v, rowp, c0i, csi, nchunks, lane);
+    else load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
+    rotate_team<N0, XG>(v, lane);
     float mx, my;
     pair_absmax2(v, mx, my);
 
@@ -161,7 +322,10 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
     double cmax = 0.0;
     if (!amax_in) {
       if (!(Aw <= 3.0e38f)) {  // non-finite input / fp32 overflow: exact loop
-        cmax = k1_slow_row_amax<F32>(rowp, 2, W, w, nchunks, a.group, a.kind, a.rot_cols);
+        if constexpr (XG)
+          cmax = k1_slow_pair_amax<F32>(rowp, c0, cstride, nchunks, a.group, a.kind, a.rot_cols);
+        else
+          cmax = k1_slow_row_amax<F32>(rowp, 2, W, w, nchunks, a.group, a.kind, a.rot_cols);
       } else if (N0 == 1) {
         cmax = (double)Aw;  // no rotation: y32 == x exactly
       } else if (Aw != 0.f) {
@@ -202,8 +366,18 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
               m |= (fabsf(v[i].y) >= thr ? 1u : 0u) << (16 + i);
             }
           }
+          if constexpr (!F32 && N0 == 64) {  // (N0 = 256: ~4% of gaussian groups pass)
+            // candidates in a group that passes the exponent-span certificate
+            // are exact as y32 * rk (no warp-cooperative double sums)
+            if (fast_cert && __any_sync(0xffffffffu, m != 0u) &&
+                group_certified_bf16<N0>(rowp, c0i, csi) && m != 0u) {
+              cmax = (double)max_nan(mx, my) * rk;
+              m = 0u;
+            }
+          }
           if (__any_sync(0xffffffffu, m != 0u))
-            cmax = k1_cands_warp<F32>(m, rowp, c0, cstride, nchunks, a.group, a.kind, a.rot_cols);
+            cmax = fmax(cmax, k1_cands_warp<F32>(m, rowp, c0, cstride, nchunks, a.group, a.kind,
+                                                 a.rot_cols));
         }
       }
     }
@@ -313,6 +487,36 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
           }
         }
       }
+      if constexpr (XG) {
+        // the lane's two chunks are adjacent: one 16-byte (packed) or 32-byte
+        // (int8) store when the row allows it
+        if (FULL || c0 < nchunks) {
+          if constexpr (BITS == 4) {
+            uint8_t* p = crow + c0 * 8;
+            if (((uintptr_t)p & 15) == 0) {
+              *reinterpret_cast<uint4*>(p) = make_uint4(wd[0][0], wd[0][1], wd[1][0], wd[1][1]);
+            } else {
+              *reinterpret_cast<uint2*>(p) = make_uint2(wd[0][0], wd[0][1]);
+              *reinterpret_cast<uint2*>(p + 8) = make_uint2(wd[1][0], wd[1][1]);
+            }
+          } else {
+            uint8_t* p = crow + c0 * 16;
+            const uint4 lo = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
+            const uint4 hi = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
+            if (((uintptr_t)p & 31) == 0) {
+              st_v8(p, lo, hi);
+            } else {
+              *reinterpret_cast<uint4*>(p) = lo;
+              *reinterpret_cast<uint4*>(p + 16) = hi;
+            }
+          }
+        } else if constexpr (BITS == 5) {  // zero-filled chunks: their codes are not stored
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) csum -= __dp4a((int)wd[h][q], 0x01010101, 0);
+        }
+      } else {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t chunk = c0 + h * cstride;
@@ -328,6 +532,7 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
         else
           *reinterpret_cast<uint4*>(crow + chunk * 16) =
               make_uint4(wd[h][0], wd[h][1], wd[h][2], wd[h][3]);
+      }
       }
       uint32_t fm = 0u;
       if (!(max_nan(max_nan(em[0], em[1]), max_nan(em[2], em[3])) <= thr))
@@ -352,8 +557,12 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
         }
       }
     } else {
-      k1_slow_row_codes<F32, BITS>(rowp, crow, 2, W, w, nchunks, invalid, scale(), a.group, a.kind,
-                                   a.rot_cols);
+      if constexpr (XG)
+        k1_slow_pair_codes<F32, BITS>(rowp, crow, c0, cstride, nchunks, invalid, scale(), a.group,
+                                      a.kind, a.rot_cols);
+      else  // (the same chunks: c0 = 32 w + lane, cstride = 32 W)
+        k1_slow_row_codes<F32, BITS>(rowp, crow, 2, W, w, nchunks, invalid, scale(), a.group,
+                                     a.kind, a.rot_cols);
       if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
     }
     if constexpr (BITS == 5) {
@@ -416,7 +625,9 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
   if constexpr (!F32 && BITS == 5) {
     if (full && !wc_off && a.codes && a.rowsum && a.s32 && !a.amax_in && !a.amax) {
-      if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;  // K = 3072, every N0 (cfg1-3)
+      // K = 3072 (cfg1-3), every N0 but 64 (whose lane-pair layout spills at
+      // the folded width: 29.0 vs 26.3 us at M = 4608)
+      if (W == 3 && N0 != 64) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
       if constexpr (N0 == 16) {  // the FLUX MLP / proj_out widths
         if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
         else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;

@@ -211,6 +211,38 @@ def test_k1_nonfinite_raises_invalid_value():
                         RotationSpec(RotationKind.regular, 16))
 
 
+@pytest.mark.parametrize("n0", [16, 64, 256])
+def test_k1_team_slow_rows(n0):
+    """Rows the fp32 path cannot certify, in the team kernel at K = 3072 (3
+    warps; for N0 >= 64 a lane pair shares a radix-4 digit, k1_team.cuh
+    rotate_team): fp32-overflowing groups settled element by element with the
+    reference's double arithmetic (group_rotate pipeline.cpp:111-151,
+    compute_scales / quantize quant.cpp:10-52), and a NaN in the last warp's
+    chunks raising InvalidValueError (quant.cpp:16-18)."""
+    M, K = 6, 3072
+    x = O.from_bf16_bits(O.synth_input(M, K, "gaussian", 11)).copy()
+    x[1, :] = 1.5 * 2.0 ** 126              # every group overflows fp32
+    x[3, 2048 + 16:2048 + 80] = -1.25 * 2.0 ** 125  # one block in warp 2
+    x[4, 5] = 1.5 * 2.0 ** 126               # a single huge element
+    xb = O.to_bf16_bits(x)
+    xv = O.from_bf16_bits(xb)
+    spec = RotationSpec(RotationKind.regular, n0)
+    rot = O.group_rotate(xv, int(spec.kind), n0)
+    sc = O.compute_scales(rot)
+    q = O.quantize(rot, sc)
+    xt = bf16_tensor(xb)
+    codes, s32, s64 = crt.rotate_quantize(xt, spec, QuantSpec(4), scales64=True)
+    assert np.array_equal(codes[:, :K // 2].cpu().numpy(), O.pack_int4_rows(q))
+    assert np.array_equal(s64.cpu().numpy(), sc)
+    c8, s8, sums = crt.rotate_quantize_i8(xt, spec)
+    assert np.array_equal(c8[:, :K].cpu().numpy().view(np.int8), q.astype(np.int8))
+    assert np.array_equal(sums.cpu().numpy(), q.astype(np.int64).sum(1))
+    xn = xt.clone()
+    xn[2, 2048 + 700] = float("nan")
+    with pytest.raises(crt.InvalidValueError):
+        crt.rotate_quantize(xn, spec)
+
+
 @pytest.mark.parametrize("spec", [
     RotationSpec(RotationKind.regular, 0),            # global group (K=1024)
     RotationSpec(RotationKind.sylvester, 32),
