@@ -105,22 +105,10 @@ __device__ __noinline__ void k1_slow_pair_codes(const void* rowp, uint8_t* crow,
 // 256) as packed 16-bit maxima of (max |x|, 0xFFFF - (min |x| - 1)).  True =>
 // every fp32 partial sum of the group's butterflies is exact.  Warp-uniform
 // call (shuffles).
+// (mx, mn: the lane's packed 16-bit max |x| and min |x| - 1 of its input
+// chunks, gathered by load_pair_xg while loading)
 template <int N0>
-__device__ __forceinline__ bool group_certified_bf16(const void* rowp, int64_t c0i, int64_t csi) {
-  const uint32_t sa = smem_u32(rowp);
-  uint32_t mx = 0u, mn = 0xFFFFFFFFu;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t ca = sa + (uint32_t)(c0i + h * csi) * 32u;
-    const uint4 t0 = ld_shared_v4(ca), t1 = ld_shared_v4(ca + 16);
-    const uint32_t u[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t m = u[i] & 0x7FFF7FFFu;
-      mx = __vmaxu2(mx, m);
-      mn = __vminu2(mn, __vsub2(m, 0x00010001u));  // zeros -> 0xFFFF
-    }
-  }
+__device__ __forceinline__ bool group_certified_bf16(uint32_t mx, uint32_t mn) {
   const uint32_t bmx = max(mx & 0xFFFFu, mx >> 16);
   const uint32_t bmn = min(mn & 0xFFFFu, mn >> 16);
   uint32_t q = (bmx << 16) | (0xFFFFu - bmn);
@@ -141,9 +129,12 @@ __device__ __forceinline__ bool group_certified_bf16(const void* rowp, int64_t c
 // lane pairs' chunks sit at 128-byte-periodic offsets {0, 32}, so the two
 // 16-byte halves are read in an order alternating with lane bit 1 (2-way
 // instead of 4-way bank conflicts, like load_pair's consecutive chunks).
-template <bool FULL>
+template <bool FULL, bool CERT>
 __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, int64_t c0i,
-                                             int64_t csi, int64_t nchunks, int lane) {
+                                             int64_t csi, int64_t nchunks, int lane, uint32_t& mx,
+                                             uint32_t& mn) {
+  mx = 0u;
+  mn = 0xFFFFFFFFu;
   const uint32_t sw = (uint32_t)(lane >> 1) & 1u;
   const uint32_t sb = smem_u32(rowp);
 #pragma unroll
@@ -157,6 +148,14 @@ __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, 
       hi = sw ? ta : tb;
     }
     const uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    if constexpr (CERT) {  // group_certified_bf16's exponent statistics
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t m = u[i] & 0x7FFF7FFFu;
+        mx = __vmaxu2(mx, m);
+        mn = __vminu2(mn, __vsub2(m, 0x00010001u));  // zeros -> 0xFFFF
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float f = __uint_as_float((i & 1) ? (u[i >> 1] & 0xFFFF0000u) : (u[i >> 1] << 16));
@@ -307,8 +306,11 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
 
     // ---- load + rotate once; per-chunk |y| maxima ---------------------------
     float2 v[16];
-    if constexpr (XG && !F32) load_pair_xg<FULL>(v, rowp, c0i, csi, nchunks, lane);
-    else load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
+    uint32_t gmx = 0u, gmn = 0u;  // exponent statistics of my input chunks (N0 = 64)
+    if constexpr (XG && !F32)
+      load_pair_xg<FULL, N0 == 64>(v, rowp, c0i, csi, nchunks, lane, gmx, gmn);
+    else
+      load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
     rotate_team<N0, XG>(v, lane);
     float mx, my;
     pair_absmax2(v, mx, my);
@@ -370,7 +372,7 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
             // candidates in a group that passes the exponent-span certificate
             // are exact as y32 * rk (no warp-cooperative double sums)
             if (fast_cert && __any_sync(0xffffffffu, m != 0u) &&
-                group_certified_bf16<N0>(rowp, c0i, csi) && m != 0u) {
+                group_certified_bf16<N0>(gmx, gmn) && m != 0u) {
               cmax = (double)max_nan(mx, my) * rk;
               m = 0u;
             }
