@@ -165,6 +165,34 @@ __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, 
   }
 }
 
+// Exact re-decision of the flagged elements (bit h*16 + i: element i of
+// chunk c0 + h*cstride) of a lane whose group passed the exponent-span
+// certificate: y32 * rk is the reference's value, so the decision is
+// quant.cpp:26-52's nearbyint(y / s) on it, lane-local.
+template <int BITS>
+__device__ __noinline__ void k1_redecide_cert(uint32_t m, const float2* vl, uint8_t* crow,
+                                              int64_t c0, int64_t cstride, int64_t nchunks,
+                                              double s, double rk) {
+  constexpr int QMAX = BITS == 8 ? 127 : 7;  // BITS 5: 4-bit codes stored as int8
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    const int i = bit & 15;
+    const int64_t chunk = c0 + (bit >> 4) * cstride;
+    if (chunk >= nchunks) continue;
+    const float y32 = (bit >> 4) ? vl[i].y : vl[i].x;
+    const int code = exact_code((double)y32 * rk, s, QMAX);
+    if constexpr (BITS == 4) {
+      uint8_t* bp = crow + chunk * 8 + (i >> 1);
+      const uint8_t old = *bp;
+      *bp = (i & 1) ? (uint8_t)((old & 0x0F) | ((code & 0x0F) << 4))
+                    : (uint8_t)((old & 0xF0) | (code & 0x0F));
+    } else {
+      crow[chunk * 16 + i] = (uint8_t)code;
+    }
+  }
+}
+
 // The team's rotation.  !XG: rotate_pair (in-chunk butterflies, outer
 // digits by xlane4).  XG (the lane-pair layout, N0 >= 64): the third radix-4 digit (element bits 4-5, the chunk's position
 // in its 4-chunk block) is split over the lane pair (lane, lane ^ 1): with
@@ -312,6 +340,10 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
     else
       load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
     rotate_team<N0, XG>(v, lane);
+    // my 64-group passes the exponent-span certificate: its y32 * 2^-3 are
+    // the reference's values (row-max candidates and near-ties settle locally)
+    bool gcert = false;
+    if constexpr (XG && !F32 && N0 == 64) gcert = fast_cert && group_certified_bf16<N0>(gmx, gmn);
     float mx, my;
     pair_absmax2(v, mx, my);
 
@@ -371,8 +403,7 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
           if constexpr (!F32 && N0 == 64) {  // (N0 = 256: ~4% of gaussian groups pass)
             // candidates in a group that passes the exponent-span certificate
             // are exact as y32 * rk (no warp-cooperative double sums)
-            if (fast_cert && __any_sync(0xffffffffu, m != 0u) &&
-                group_certified_bf16<N0>(gmx, gmn) && m != 0u) {
+            if (gcert && m != 0u) {
               cmax = (double)max_nan(mx, my) * rk;
               m = 0u;
             }
@@ -549,6 +580,16 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
           if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
         }
       } else {
+        if constexpr (XG && !F32 && N0 == 64) {
+          if (gcert && fm != 0u) {
+            float2 vl[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vl[i] = v[i];
+            k1_redecide_cert<BITS>(fm, vl, crow, c0, cstride, nchunks, scale(), rk);
+            fm = 0u;
+            if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
+          }
+        }
         if (__any_sync(0xffffffffu, fm != 0u)) {
           k1_redecide<F32, BITS>(fm, rowp, crow, c0, cstride, nchunks, scale(), a.group, a.kind,
                                  a.rot_cols);
