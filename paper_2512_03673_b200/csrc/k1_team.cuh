@@ -165,6 +165,61 @@ __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, 
   }
 }
 
+// Sum certificate of the N0 = 256 groups of a chunk pair (bf16 inputs v,
+// before the rotation).  Every value the butterflies form -- any stage's
+// output, xlane4's partial sums, rotate_team's u -- is a +-1 combination of
+// a subset of the group's inputs, so its magnitude is at most S = sum |x|,
+// and all are integer multiples of the smallest nonzero input's bf16 ulp
+// 2^(E_min - 134) (E_min its biased exponent).  S <= 2^24 ulps => every
+// fp32 operation is exact.  S is accumulated in fp32 (relative error < 2^-16
+// for 256 terms), so the test is S <= 2^(E_min - 110) (1 - 2^-12).  inf / NaN
+// fail the comparison; subnormal inputs are excluded.  For gaussian rows
+// ~50% of the groups pass (the exponent-span test: ~4%).  Returns the bits
+// (h*16 + i) of the certified chunks.  Groups: XG -- both chunks of the lane
+// in one group over lane bits 0-2; otherwise chunk h's group is the 16 lanes
+// sharing lane bit 4.  Warp-uniform call (shuffles).
+template <bool XG>
+__device__ __forceinline__ uint32_t group_sum_certified_256(const float2 (&v)[16]) {
+  float2 sa = make_float2(0.f, 0.f);
+  uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;  // min |x| bits - 1 (zeros -> top)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 a = make_float2(fabsf(v[i].x), fabsf(v[i].y));
+    sa = __fadd2_rn(sa, a);
+    m0 = min(m0, __float_as_uint(a.x) - 1u);
+    m1 = min(m1, __float_as_uint(a.y) - 1u);
+  }
+  float s0 = sa.x, s1 = sa.y;
+  if constexpr (XG) {
+    s0 += s1;
+    m0 = min(m0, m1);
+#pragma unroll
+    for (int o = 1; o <= 4; o <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      m0 = min(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    }
+    s1 = s0;
+    m1 = m0;
+  } else {
+#pragma unroll
+    for (int o = 1; o <= 8; o <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      m0 = min(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+      m1 = min(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+  }
+  auto ok = [](float s, uint32_t mm) {
+    const uint32_t b = mm + 1u;  // smallest nonzero |x| bits; 0: all zero
+    if (b == 0u) return true;    // all-zero group: y = 0
+    if (b < 0x00800000u) return false;  // subnormal input
+    const uint32_t e = b >> 23;         // E_min (<= 254: inf / NaN fail below)
+    if (e > 237u) return false;         // bound not representable
+    return s <= __uint_as_float((e + 17u) << 23) * 0.999755859375f;
+  };
+  return (ok(s0, m0) ? 0x0000FFFFu : 0u) | (ok(s1, m1) ? 0xFFFF0000u : 0u);
+}
+
 // Exact re-decision of the flagged elements (bit h*16 + i: element i of
 // chunk c0 + h*cstride) of a lane whose group passed the exponent-span
 // certificate: y32 * rk is the reference's value, so the decision is
@@ -251,12 +306,12 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.K / 16;
-  // my (output) chunks c0 and c0 + cstride; inputs c0i and c0i + csi.  The
-  // lane-pair layout (rotate_team) is chosen per instantiation as measured:
-  // N0 = 64 always (26.3 vs 28.1 us at M = 4608, K = 3072; 92.9 vs 105.8 at
-  // K = 12288); N0 = 256 in the runtime-width kernel (148 vs 155 us at K =
-  // 12288) but not at the folded W = 3, where it spills (43.4 vs 41.4 us).
-  constexpr bool XG = N0 == 64 || (N0 == 256 && WC == 0);
+  // my (output) chunks c0 and c0 + cstride; inputs c0i and c0i + csi (the
+  // lane-pair layout of rotate_team for N0 >= 64, which the launcher runs
+  // only at runtime width: folded, it spills)
+  constexpr bool XG = N0 >= 64;
+  // lane-local settlement of certified groups (N0 >= 64, bf16 rows)
+  constexpr bool CERTG = !F32 && N0 >= 64;
   const int64_t gl = (int64_t)w * 32 + lane;
   const int64_t cstride = XG ? 1 : (int64_t)W * 32;
   const int64_t c0 = XG ? 4 * (gl >> 1) + 2 * (lane & 1) : gl;
@@ -339,11 +394,17 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
       load_pair_xg<FULL, N0 == 64>(v, rowp, c0i, csi, nchunks, lane, gmx, gmn);
     else
       load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
-    rotate_team<N0, XG>(v, lane);
-    // my 64-group passes the exponent-span certificate: its y32 * 2^-3 are
-    // the reference's values (row-max candidates and near-ties settle locally)
+    // cmask: the bits (h*16 + i) of my pair whose group passes a certificate
+    // (every fp32 partial sum exact), so their y32 * rk are the reference's
+    // values: row-max candidates and near-ties there settle lane-locally
+    // (N0 = 64: one group per lane, gcert)
+    uint32_t cmask = 0u;
     bool gcert = false;
-    if constexpr (XG && !F32 && N0 == 64) gcert = fast_cert && group_certified_bf16<N0>(gmx, gmn);
+    if constexpr (CERTG && N0 == 256) {
+      if (fast_cert) cmask = group_sum_certified_256<XG>(v);
+    }
+    rotate_team<N0, XG>(v, lane);
+    if constexpr (CERTG && N0 == 64) gcert = fast_cert && group_certified_bf16<N0>(gmx, gmn);
     float mx, my;
     pair_absmax2(v, mx, my);
 
@@ -400,11 +461,16 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
               m |= (fabsf(v[i].y) >= thr ? 1u : 0u) << (16 + i);
             }
           }
-          if constexpr (!F32 && N0 == 64) {  // (N0 = 256: ~4% of gaussian groups pass)
-            // candidates in a group that passes the exponent-span certificate
-            // are exact as y32 * rk (no warp-cooperative double sums)
+          if constexpr (CERTG && N0 == 64) {
             if (gcert && m != 0u) {
               cmax = (double)max_nan(mx, my) * rk;
+              m = 0u;
+            }
+          } else if constexpr (CERTG) {
+            // candidates all in certified groups are exact as y32 * rk (no
+            // warp-cooperative double sums); mx / my are the chunk maxima
+            if (m != 0u && (m & ~cmask) == 0u) {
+              cmax = (double)fmaxf((m & 0xFFFFu) ? mx : 0.f, (m >> 16) ? my : 0.f) * rk;
               m = 0u;
             }
           }
@@ -580,13 +646,22 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
           if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
         }
       } else {
-        if constexpr (XG && !F32 && N0 == 64) {
+        if constexpr (CERTG && N0 == 64) {
           if (gcert && fm != 0u) {
             float2 vl[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) vl[i] = v[i];
             k1_redecide_cert<BITS>(fm, vl, crow, c0, cstride, nchunks, scale(), rk);
             fm = 0u;
+            if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
+          }
+        } else if constexpr (CERTG) {
+          if ((fm & cmask) != 0u) {
+            float2 vl[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) vl[i] = v[i];
+            k1_redecide_cert<BITS>(fm & cmask, vl, crow, c0, cstride, nchunks, scale(), rk);
+            fm &= ~cmask;
             if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
           }
         }
@@ -668,9 +743,11 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
   if constexpr (!F32 && BITS == 5) {
     if (full && !wc_off && a.codes && a.rowsum && a.s32 && !a.amax_in && !a.amax) {
-      // K = 3072 (cfg1-3), every N0 but 64 (whose lane-pair layout spills at
-      // the folded width: 29.0 vs 26.3 us at M = 4608)
-      if (W == 3 && N0 != 64) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
+      // K = 3072 (cfg1-3), N0 <= 16 (the N0 >= 64 lane-pair layout spills at
+      // the folded width: N0 = 64 29.0 vs 26.3 us, 256 38.9 vs 38.4 at M = 4608)
+      if constexpr (N0 <= 16) {
+        if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
+      }
       if constexpr (N0 == 16) {  // the FLUX MLP / proj_out widths
         if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
         else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
