@@ -99,42 +99,13 @@ __device__ __noinline__ void k1_slow_pair_codes(const void* rowp, uint8_t* crow,
   }
 }
 
-// Exponent-span certificate of a whole lane-pair-layout group (chunk_certified_bf16's
-// test): the calling lane's input chunks c0i, c0i + csi, combined over the
-// group's lanes (rotate_team's layout: lane bit 0 for N0 = 64, bits 0-2 for
-// 256) as packed 16-bit maxima of (max |x|, 0xFFFF - (min |x| - 1)).  True =>
-// every fp32 partial sum of the group's butterflies is exact.  Warp-uniform
-// call (shuffles).
-// (mx, mn: the lane's packed 16-bit max |x| and min |x| - 1 of its input
-// chunks, gathered by load_pair_xg while loading)
-template <int N0>
-__device__ __forceinline__ bool group_certified_bf16(uint32_t mx, uint32_t mn) {
-  const uint32_t bmx = max(mx & 0xFFFFu, mx >> 16);
-  const uint32_t bmn = min(mn & 0xFFFFu, mn >> 16);
-  uint32_t q = (bmx << 16) | (0xFFFFu - bmn);
-  q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 1));
-  if constexpr (N0 >= 256) {
-    q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 2));
-    q = __vmaxu2(q, __shfl_xor_sync(0xffffffffu, q, 4));
-  }
-  const uint32_t bmax = q >> 16;
-  const uint32_t bmin = (0xFFFFu - (q & 0xFFFFu)) + 1u;  // 0x10000: all zero
-  if (bmax == 0u) return true;                          // all-zero group: y = 0
-  if (bmax >= 0x7F80u || bmin < 0x0080u) return false;  // inf/NaN or subnormal
-  constexpr int L2 = N0 == 64 ? 6 : 8;
-  return 1 + L2 + (int)((bmax >> 7) - (bmin >> 7)) + 8 <= 24;
-}
-
 // rotate_team's input chunks in the lane-pair layout (bf16 rows in shared memory): the
 // lane pairs' chunks sit at 128-byte-periodic offsets {0, 32}, so the two
 // 16-byte halves are read in an order alternating with lane bit 1 (2-way
 // instead of 4-way bank conflicts, like load_pair's consecutive chunks).
-template <bool FULL, bool CERT>
+template <bool FULL>
 __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, int64_t c0i,
-                                             int64_t csi, int64_t nchunks, int lane, uint32_t& mx,
-                                             uint32_t& mn) {
-  mx = 0u;
-  mn = 0xFFFFFFFFu;
+                                             int64_t csi, int64_t nchunks, int lane) {
   const uint32_t sw = (uint32_t)(lane >> 1) & 1u;
   const uint32_t sb = smem_u32(rowp);
 #pragma unroll
@@ -148,14 +119,6 @@ __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, 
       hi = sw ? ta : tb;
     }
     const uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    if constexpr (CERT) {  // group_certified_bf16's exponent statistics
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t m = u[i] & 0x7FFF7FFFu;
-        mx = __vmaxu2(mx, m);
-        mn = __vminu2(mn, __vsub2(m, 0x00010001u));  // zeros -> 0xFFFF
-      }
-    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float f = __uint_as_float((i & 1) ? (u[i >> 1] & 0xFFFF0000u) : (u[i >> 1] << 16));
@@ -165,21 +128,20 @@ __device__ __forceinline__ void load_pair_xg(float2 (&v)[16], const void* rowp, 
   }
 }
 
-// Sum certificate of the N0 = 256 groups of a chunk pair (bf16 inputs v,
-// before the rotation).  Every value the butterflies form -- any stage's
-// output, xlane4's partial sums, rotate_team's u -- is a +-1 combination of
-// a subset of the group's inputs, so its magnitude is at most S = sum |x|,
-// and all are integer multiples of the smallest nonzero input's bf16 ulp
-// 2^(E_min - 134) (E_min its biased exponent).  S <= 2^24 ulps => every
-// fp32 operation is exact.  S is accumulated in fp32 (relative error < 2^-16
-// for 256 terms), so the test is S <= 2^(E_min - 110) (1 - 2^-12).  inf / NaN
-// fail the comparison; subnormal inputs are excluded.  For gaussian rows
-// ~50% of the groups pass (the exponent-span test: ~4%).  Returns the bits
-// (h*16 + i) of the certified chunks.  Groups: XG -- both chunks of the lane
-// in one group over lane bits 0-2; otherwise chunk h's group is the 16 lanes
-// sharing lane bit 4.  Warp-uniform call (shuffles).
-template <bool XG>
-__device__ __forceinline__ uint32_t group_sum_certified_256(const float2 (&v)[16]) {
+// Sum certificate of the calling lane's group (lane-pair layout: both of its
+// chunks lie in one group spanning lane bits 0 .. log2(N0 / 32) - 1), from
+// the bf16 inputs v before the rotation.  Every value the butterflies form
+// -- any stage's output, xlane4's partial sums, rotate_team's u -- is a +-1
+// combination of a subset of the group's inputs, so its magnitude is at
+// most S = sum |x|, and all are integer multiples of the smallest nonzero
+// input's bf16 ulp 2^(E_min - 134) (E_min its biased exponent).  S <= 2^24
+// ulps => every fp32 operation is exact.  S is accumulated in fp32 (relative
+// error < 2^-16 for 256 terms), so the test is S <= 2^(E_min - 110) (1 -
+// 2^-12).  inf / NaN fail the comparison; subnormal inputs are excluded.
+// Gaussian rows: ~95% of 64-groups and ~50% of 256-groups pass (the
+// exponent-span test: 82% / 4%).  Warp-uniform call (shuffles).
+template <int N0>
+__device__ __forceinline__ bool group_sum_certified(const float2 (&v)[16]) {
   float2 sa = make_float2(0.f, 0.f);
   uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;  // min |x| bits - 1 (zeros -> top)
 #pragma unroll
@@ -189,35 +151,19 @@ __device__ __forceinline__ uint32_t group_sum_certified_256(const float2 (&v)[16
     m0 = min(m0, __float_as_uint(a.x) - 1u);
     m1 = min(m1, __float_as_uint(a.y) - 1u);
   }
-  float s0 = sa.x, s1 = sa.y;
-  if constexpr (XG) {
-    s0 += s1;
-    m0 = min(m0, m1);
+  float s = sa.x + sa.y;
+  uint32_t m = min(m0, m1);
 #pragma unroll
-    for (int o = 1; o <= 4; o <<= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      m0 = min(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-    }
-    s1 = s0;
-    m1 = m0;
-  } else {
-#pragma unroll
-    for (int o = 1; o <= 8; o <<= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      m0 = min(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-      m1 = min(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-    }
+  for (int o = 1; o < N0 / 32; o <<= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
   }
-  auto ok = [](float s, uint32_t mm) {
-    const uint32_t b = mm + 1u;  // smallest nonzero |x| bits; 0: all zero
-    if (b == 0u) return true;    // all-zero group: y = 0
-    if (b < 0x00800000u) return false;  // subnormal input
-    const uint32_t e = b >> 23;         // E_min (<= 254: inf / NaN fail below)
-    if (e > 237u) return false;         // bound not representable
-    return s <= __uint_as_float((e + 17u) << 23) * 0.999755859375f;
-  };
-  return (ok(s0, m0) ? 0x0000FFFFu : 0u) | (ok(s1, m1) ? 0xFFFF0000u : 0u);
+  const uint32_t b = m + 1u;          // smallest nonzero |x| bits; 0: all zero
+  if (b == 0u) return true;           // all-zero group: y = 0
+  if (b < 0x00800000u) return false;  // subnormal input
+  const uint32_t e = b >> 23;         // E_min (inf / NaN fail the comparison)
+  if (e > 237u) return false;         // bound not representable
+  return s <= __uint_as_float((e + 17u) << 23) * 0.999755859375f;
 }
 
 // Exact re-decision of the flagged elements (bit h*16 + i: element i of
@@ -389,9 +335,8 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
 
     // ---- load + rotate once; per-chunk |y| maxima ---------------------------
     float2 v[16];
-    uint32_t gmx = 0u, gmn = 0u;  // exponent statistics of my input chunks (N0 = 64)
     if constexpr (XG && !F32)
-      load_pair_xg<FULL, N0 == 64>(v, rowp, c0i, csi, nchunks, lane, gmx, gmn);
+      load_pair_xg<FULL>(v, rowp, c0i, csi, nchunks, lane);
     else
       load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
     // cmask: the bits (h*16 + i) of my pair whose group passes a certificate
@@ -401,10 +346,10 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
     uint32_t cmask = 0u;
     bool gcert = false;
     if constexpr (CERTG && N0 == 256) {
-      if (fast_cert) cmask = group_sum_certified_256<XG>(v);
+      if (fast_cert) cmask = group_sum_certified<N0>(v) ? 0xFFFFFFFFu : 0u;
     }
+    if constexpr (CERTG && N0 == 64) gcert = fast_cert && group_sum_certified<N0>(v);
     rotate_team<N0, XG>(v, lane);
-    if constexpr (CERTG && N0 == 64) gcert = fast_cert && group_certified_bf16<N0>(gmx, gmn);
     float mx, my;
     pair_absmax2(v, mx, my);
 

@@ -8,6 +8,7 @@ and on the bytes the int8-code layout actually moves (2 + 1 B + 8 B/row).
 python tools/k1_bench.py [M K N0 bits] ...   (default: the FLUX shapes)
 """
 import ctypes
+import gc
 import json
 import sys
 
@@ -69,6 +70,13 @@ def k1_time(M, K, n0, bits=5, reps=6):
         b.synchronize()
         ts.append(a.elapsed_time(b) * 1e3 / n)
     us = sorted(ts)[len(ts) // 2]
+    # release this graph and its buffers now: a second capture of the same
+    # shape while they linger ran 10-25x slower (graph replays only; eager
+    # launches are unaffected)
+    del graph, xs, codes, s32, sums
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     packed = M * K * 2.5 + 4 * M
     moved = M * K * (3 if bits != 4 else 2.5) + (8 if bits == 5 else 4) * M
     return {"M": M, "K": K, "n0": n0, "bits": bits, "us": round(us, 2),
