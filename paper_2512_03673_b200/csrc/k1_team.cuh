@@ -253,8 +253,7 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = a.K / 16;
   // my (output) chunks c0 and c0 + cstride; inputs c0i and c0i + csi (the
-  // lane-pair layout of rotate_team for N0 >= 64, which the launcher runs
-  // only at runtime width: folded, it spills)
+  // lane-pair layout of rotate_team for N0 >= 64)
   constexpr bool XG = N0 >= 64;
   // lane-local settlement of certified groups (N0 >= 64, bf16 rows)
   constexpr bool CERTG = !F32 && N0 >= 64;
@@ -688,11 +687,9 @@ cudaError_t launch_team(const K1Args& a0, cudaStream_t st, int64_t* launches) {
   int ki = full ? 1 : 0;  // which kernel (its smem attribute is cached per kernel)
   if constexpr (!F32 && BITS == 5) {
     if (full && !wc_off && a.codes && a.rowsum && a.s32 && !a.amax_in && !a.amax) {
-      // K = 3072 (cfg1-3), N0 <= 16 (the N0 >= 64 lane-pair layout spills at
-      // the folded width: N0 = 64 29.0 vs 26.3 us, 256 38.9 vs 38.4 at M = 4608)
-      if constexpr (N0 <= 16) {
-        if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
-      }
+      // K = 3072 (cfg1-3), every N0 (M = 4608, N0 = 64 / 256: 20.3 / 35.6 us
+      // vs 20.4 / 38.1 at runtime width)
+      if (W == 3) kern = k1_team<N0, F32, BITS, true, 3>, ki = 2;
       if constexpr (N0 == 16) {  // the FLUX MLP / proj_out widths
         if (W == 12) kern = k1_team<N0, F32, BITS, true, 12>, ki = 3;
         else if (W == 15) kern = k1_team<N0, F32, BITS, true, 15>, ki = 4;
