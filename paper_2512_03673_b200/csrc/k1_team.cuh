@@ -338,16 +338,11 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
       load_pair_xg<FULL>(v, rowp, c0i, csi, nchunks, lane);
     else
       load_pair<F32, true, FULL>(v, rowp, c0i, csi, nchunks);
-    // cmask: the bits (h*16 + i) of my pair whose group passes a certificate
-    // (every fp32 partial sum exact), so their y32 * rk are the reference's
-    // values: row-max candidates and near-ties there settle lane-locally
-    // (N0 = 64: one group per lane, gcert)
-    uint32_t cmask = 0u;
+    // gcert: my group (both chunks of the pair, N0 >= 64) passes the sum
+    // certificate (every fp32 partial sum exact), so its y32 * rk are the
+    // reference's values: row-max candidates and near-ties settle lane-locally
     bool gcert = false;
-    if constexpr (CERTG && N0 == 256) {
-      if (fast_cert) cmask = group_sum_certified<N0>(v) ? 0xFFFFFFFFu : 0u;
-    }
-    if constexpr (CERTG && N0 == 64) gcert = fast_cert && group_sum_certified<N0>(v);
+    if constexpr (CERTG) gcert = fast_cert && group_sum_certified<N0>(v);
     rotate_team<N0, XG>(v, lane);
     float mx, my;
     pair_absmax2(v, mx, my);
@@ -405,16 +400,11 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
               m |= (fabsf(v[i].y) >= thr ? 1u : 0u) << (16 + i);
             }
           }
-          if constexpr (CERTG && N0 == 64) {
+          if constexpr (CERTG) {
+            // candidates of a certified group are exact as y32 * rk (no
+            // warp-cooperative double sums)
             if (gcert && m != 0u) {
               cmax = (double)max_nan(mx, my) * rk;
-              m = 0u;
-            }
-          } else if constexpr (CERTG) {
-            // candidates all in certified groups are exact as y32 * rk (no
-            // warp-cooperative double sums); mx / my are the chunk maxima
-            if (m != 0u && (m & ~cmask) == 0u) {
-              cmax = (double)fmaxf((m & 0xFFFFu) ? mx : 0.f, (m >> 16) ? my : 0.f) * rk;
               m = 0u;
             }
           }
@@ -590,22 +580,13 @@ __global__ void __maxnreg__(WC == 15 ? 128 : kK1TRegs) k1_team(K1Args a) {
           if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
         }
       } else {
-        if constexpr (CERTG && N0 == 64) {
+        if constexpr (CERTG) {
           if (gcert && fm != 0u) {
             float2 vl[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) vl[i] = v[i];
             k1_redecide_cert<BITS>(fm, vl, crow, c0, cstride, nchunks, scale(), rk);
             fm = 0u;
-            if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
-          }
-        } else if constexpr (CERTG) {
-          if ((fm & cmask) != 0u) {
-            float2 vl[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) vl[i] = v[i];
-            k1_redecide_cert<BITS>(fm & cmask, vl, crow, c0, cstride, nchunks, scale(), rk);
-            fm &= ~cmask;
             if constexpr (BITS == 5) csum = reread_pair_sum<FULL>(crow, c0, cstride, nchunks);
           }
         }
